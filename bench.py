@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""APT stencil-update throughput of the B200 hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One bench "step" = one hybrid_solve pass of n_apt accelerated pseudo-transient
+steps (time hybrid_solve with n_pt = 0) over the 3D cantilever
+C5 grid (512 x 256 x 256 nodes, single material, FP64), inputs resident in HBM.
+value = nodes * n_apt * K / device time (GLUPS, whole job).  e2e = the same
+through the C-ABI with host buffers: every step uploads the state history from
+pinned host memory, solves, and downloads it.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+built from /root/reference with OpenMP, all host threads) on a bounded sample
+of the same workload; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "APT stencil updates/s (GLUPS) and % HBM roofline at 1/2/4/8 B200 vs host-CPU"
+UNIT = "GLUPS"
+APT_BYTES_PER_NODE = 80.0  # u_n 24 + u_{n-1} 24 + E 8 + u_{n+1} 24
+
+
+def args_():
+    a = argparse.ArgumentParser()
+    a.add_argument("--gpus", type=int, default=1)
+    a.add_argument("--steps", type=int, default=10)
+    a.add_argument("--warmup", type=int, default=3)
+    a.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    a.add_argument("--config", default="C5")
+    a.add_argument("--n-apt", type=int, default=100)
+    a.add_argument("--no-e2e", action="store_true")
+    a.add_argument("--no-cpu", action="store_true")
+    a.add_argument("--cpu-steps", type=int, default=2, help="APT steps in the CPU baseline sample")
+    return a.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def workload(name):
+    """Assemble the configured problem exactly as the reference's build_problem would."""
+    from paper_2509_06971_b200 import device as D
+    from paper_2509_06971_b200 import problem as P
+
+    cfg = P.config(name)
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=D.spectral_bound)
+    g = prob.grid
+    N = g.num_nodes
+    # interpolate_into (objectives.hpp:95-116) of the initial design
+    E = np.zeros(N)
+    for i, p in enumerate(prob.properties):
+        E += p * prob.initial_phases[i * N:(i + 1) * N] ** 3
+    E = np.maximum(E, prob.void_floor)
+    return cfg, prob, sched, E
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(name, prob, sched, E, steps, kind_pref="reference"):
+    """The reference's own OpenMP CPU path (oracle/_ref) on a bounded sample."""
+    from oracle import oracle as O
+    from paper_2509_06971_b200 import problem as P
+
+    if kind_pref == "reference" and O.has_reference():
+        orc, kind, cores = O.load("reference"), "reference", host_threads()
+        orc.set_threads(cores)
+    else:
+        orc, kind, cores = O.load("port"), "port", 1
+    g = prob.grid
+    p = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, steps, 0, sched.pt.form)
+    sec = orc.time_hybrid(1, g, prob.bc, E, prob.poisson_ratio, prob.source, prob.initial_state,
+                          prob.initial_state, p)
+    value = g.num_nodes * steps / sec / 1e9
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{steps} APT steps of {name} ({g.n[0]}x{g.n[1]}x{g.n[2]}), {sec:.2f} s"}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg, prob, sched, E = workload(a.config)
+    g = prob.grid
+    vals = []
+    from oracle import oracle as O
+
+    if not O.has_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return 0
+    for it in range(a.warmup + a.steps):
+        cb = cpu_baseline(a.config, prob, sched, E, 1)
+        if it >= a.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": g.num_nodes / (v * 1e9) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem)",
+        "config": {"workload": f"{a.config}: {cfg.nx}x{cfg.ny}x{cfg.nz} cantilever3d elasticity, APT steps",
+                   "sample": "1 APT step per bench step"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
+                         "sample": "1 APT step of the full grid per bench step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(a):
+    import torch
+
+    from paper_2509_06971_b200 import device as D
+    from paper_2509_06971_b200 import problem as P
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    cfg, prob, sched, E = workload(a.config)
+    g = prob.grid
+    N = g.num_nodes
+    comps = prob.comps
+    ctx = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local)
+    ctx.set_constraints(prob.cons_entry, prob.cons_value)
+    ctx.set_source(prob.source)
+    ctx.set_property(E)
+    ctx.init_operator()
+    ctx.set_state(prob.initial_state, prob.initial_state)
+    params = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, a.n_apt, 0, sched.pt.form)
+
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    for _ in range(a.warmup):
+        ctx.hybrid_solve(params)
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    ctx.kernel_timing(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            ctx.hybrid_solve(params)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    kms, klaunch, kbytes, kname = ctx.kernel_stats()
+    ctx.kernel_timing(False)
+    launches = ctx.launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    total_updates = N * a.n_apt * a.steps * world
+    value = total_updates / (ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    avg_launch_s = kms * 1e-3 / max(klaunch, 1)
+    achieved = N * APT_BYTES_PER_NODE / avg_launch_s / 1e9
+
+    # e2e: the same hybrid_solve through the C-ABI with host buffers
+    e2e = None
+    if not a.no_e2e:
+        host_cur = torch.empty(comps * N, dtype=torch.float64, pin_memory=True).numpy()
+        host_prev = torch.empty(comps * N, dtype=torch.float64, pin_memory=True).numpy()
+        host_cur[:] = prob.initial_state
+        host_prev[:] = prob.initial_state
+        e2e_steps = max(2, min(a.steps, 5))
+
+        def e2e_step():
+            ctx.set_state(host_cur, host_prev)
+            ctx.hybrid_solve(params)
+            c, p = ctx.get_state()
+            host_cur[:] = c
+            host_prev[:] = p
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": N * a.n_apt * e2e_steps * world / dt / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * comps * N * 8, "d2h_bytes_per_step": 2 * comps * N * 8,
+               "steps": e2e_steps}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            d = json.load(f)
+        traffic = d.get(kname, {}).get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem: initial design, zero state)",
+        "config": {"workload": f"{a.config}: {g.n[0]}x{g.n[1]}x{g.n[2]} cantilever3d elasticity "
+                               f"({N} nodes), hybrid_solve with n_apt={a.n_apt}, n_pt=0, "
+                               f"form={'semi_implicit' if sched.pt.form else 'explicit'}",
+                   "l2": "inputs larger than L2 (state 2x805 MB + modulus 268 MB per step)",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} GPUs"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": kname, "peak_source": peak_kind,
+                     "bytes_per_node": APT_BYTES_PER_NODE, "avg_launch_ms": avg_launch_s * 1e3},
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not a.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(a.config, prob, sched, E, a.cpu_steps)
+        except Exception as ex:  # noqa: BLE001
+            line["cpu_baseline"] = {"error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    a = args_()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -327,6 +327,16 @@ class Oracle:
                                        _dp(source), _dp(cur), _dp(prev), C.byref(params), C.byref(step))
         return rc, cur, prev, step.value
 
+    def time_hybrid(self, physics, grid, bc, prop, nu, source, cur, prev, params):
+        """Seconds spent inside hybrid_solve alone (operator set-up excluded)."""
+        grid, bc, params = grid_struct(grid), bc_struct(bc), pt_struct(params)
+        cur = np.array(cur, dtype=np.float64, copy=True)
+        prev = np.array(prev, dtype=np.float64, copy=True)
+        sec = C.c_double(0.0)
+        self._check(self.lib.orc_time_hybrid(physics, C.byref(grid.c), C.byref(bc.c), _dp(prop), C.c_double(nu),
+                                             _dp(source), _dp(cur), _dp(prev), C.byref(params), C.byref(sec)))
+        return sec.value
+
     def iterate_to_tolerance(self, physics, grid, bc, prop, nu, source, cur, prev, mode, params,
                              target, max_iters):
         grid, bc, params = grid_struct(grid), bc_struct(bc), pt_struct(params)

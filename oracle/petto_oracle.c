@@ -11,7 +11,9 @@
  */
 #include "petto_oracle.h"
 
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
+#include <time.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -643,6 +645,26 @@ int orc_hybrid_solve(int physics, const orc_grid* o, const orc_bc* bc, const dou
     double* r = (double*)malloc(sizeof(double) * (size_t)n);
     hist_t h = {cur, prev};
     rc = hybrid_solve(&h, &op, p, r, abort_step);
+    hist_writeback(&h, cur, prev, NULL, NULL, n);
+    free(r);
+    op_free(&op);
+    return rc;
+}
+
+int orc_time_hybrid(int physics, const orc_grid* o, const orc_bc* bc, const double* property, double nu,
+                    const double* source, double* cur, double* prev, const orc_pt_params* p,
+                    double* seconds) {
+    op_t op;
+    int rc = op_init(&op, physics, o, bc, property, nu, source);
+    if (rc) return rc;
+    const int64_t n = nnodes(&op.g) * op.comps;
+    double* r = (double*)malloc(sizeof(double) * (size_t)n);
+    hist_t h = {cur, prev};
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    rc = hybrid_solve(&h, &op, p, r, NULL);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
     hist_writeback(&h, cur, prev, NULL, NULL, n);
     free(r);
     op_free(&op);

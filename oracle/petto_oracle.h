@@ -161,6 +161,11 @@ double orc_residual_norm(const double* r, int64_t nodes, int comps);
 int orc_hybrid_solve(int physics, const orc_grid* g, const orc_bc* bc, const double* property,
                      double nu, const double* source, double* cur, double* prev,
                      const orc_pt_params* p, int64_t* abort_step);
+/* hybrid_solve timed alone (operator construction excluded): wall seconds of the
+ * solve itself, for the CPU baseline legs of bench.py. */
+int orc_time_hybrid(int physics, const orc_grid* g, const orc_bc* bc, const double* property,
+                    double nu, const double* source, double* cur, double* prev,
+                    const orc_pt_params* p, double* seconds);
 int orc_iterate_to_tolerance(int physics, const orc_grid* g, const orc_bc* bc,
                              const double* property, double nu, const double* source,
                              double* cur, double* prev, int mode /*0 PT, 1 APT*/,

@@ -11,6 +11,7 @@
 // BoundarySpec / Field objects from the POD arguments, call the reference entry
 // point named in the comment, copy results back.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <sstream>
@@ -240,6 +241,20 @@ int orc_hybrid_solve(int physics, const orc_grid* g, const orc_bc* b, const doub
     });
     delete keep;
     return rc;
+}
+
+int orc_time_hybrid(int physics, const orc_grid* g, const orc_bc* b, const double* property, double nu,
+                    const double* source, double* cur, double* prev, const orc_pt_params* p, double* seconds) {
+    return guarded([&] {
+        OpBundle ob(physics, g, b, property, nu, source);
+        const int comps = ob.op->components();
+        StateHistory<double> hist(field_from(ob.grid, comps, cur), field_from(ob.grid, comps, prev));
+        const auto t0 = std::chrono::steady_clock::now();
+        hybrid_solve(hist, *ob.op, make_params(p));
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        field_to(hist.current, cur);
+        field_to(hist.previous, prev);
+    });
 }
 
 int orc_iterate_to_tolerance(int physics, const orc_grid* g, const orc_bc* b,

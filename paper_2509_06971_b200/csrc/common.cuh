@@ -1,0 +1,181 @@
+// common.cuh -- device-side layout, arithmetic and sm_100a PTX helpers.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace petto_b200 {
+
+// HBM layout of one rank's fields.  Rows are padded to a pitch of px doubles
+// (px % 16 == 0) so every TMA global stride is 16-byte aligned; the rank stores
+// global node planes [ks0, ks0 + nzs) (owned planes [kb, ke) plus one ghost
+// plane per interior slab face).  Component c of a vector field starts at c*Ns.
+struct Geo {
+    int dim;
+    int nx, ny, nz;  // global node counts (nz = 1 in 2D)
+    int kb, ke;      // owned global planes
+    int ks0, nzs;    // stored planes
+    int px;          // row pitch (elements)
+    long long Ns;    // stored nodes incl. padding = px * ny * nzs
+    double h[3];
+};
+
+// Device-resident control block of a context: non-finite detection with the
+// reference's check_finite cadence (state_solver.hpp:463-497) and the
+// iterate_to_tolerance stop logic (:511-541), evaluated on the device so the
+// step loops never synchronise with the host.
+struct DeviceStatus {
+    unsigned flags;        // bit 0 non-finite written, bit 1 non-positive kappa
+    int done;              // iterate_to_tolerance: stop flag
+    long long first_bad;   // first step that wrote a non-finite value (LLONG_MAX: none)
+    int converged;
+    int aborted;
+    long long iter;        // iterate_to_tolerance: index of the residual being evaluated
+    long long iterations;
+    double r_initial, r_final;
+    double target;
+    long long max_iters;
+    double nodes;
+    double sumsq;
+};
+
+#define PETTO_NO_BAD 0x7fffffffffffffffLL
+
+// True when the kernel of pseudo-time step `step` (1-based) must not run: the
+// reference would already have aborted at the check_finite following the first
+// non-finite write (every 100 steps and at the last step), or the tolerance
+// loop has stopped.
+__device__ __forceinline__ bool skip_step(const DeviceStatus* s, long long step, long long nsteps) {
+    if (s->done) return true;
+    const long long fb = s->first_bad;
+    if (fb == PETTO_NO_BAD) return false;
+    long long lim = ((fb + 99) / 100) * 100;
+    if (lim > nsteps) lim = nsteps;
+    return step > lim;
+}
+
+__device__ __forceinline__ void mark_bad(DeviceStatus* s, long long step) {
+    atomicOr(&s->flags, 1u);
+    atomicMin(reinterpret_cast<unsigned long long*>(&s->first_bad), (unsigned long long)step);
+}
+
+__host__ __device__ inline long long lidx(const Geo& g, int i, int j, int k) {
+    return ((long long)(k - g.ks0) * g.ny + j) * g.px + i;
+}
+
+// Round-to-nearest IEEE operations that the compiler never contracts into FMA:
+// the replica kernels spell the reference's expressions with these.
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Lumped extent along an axis (grid.hpp:64-67).
+__device__ __forceinline__ double cell_extent(const Geo& g, int axis, int i) {
+    const int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
+    if (n == 1) return 1.0;
+    return (i == 0 || i == n - 1) ? rmul(0.5, g.h[axis]) : g.h[axis];
+}
+
+// cell_volume (grid.hpp:69-73), reference multiplication order.
+__device__ __forceinline__ double cell_volume(const Geo& g, int i, int j, int k) {
+    double v = rmul(cell_extent(g, 0, i), cell_extent(g, 1, j));
+    if (g.dim == 3) v = rmul(v, cell_extent(g, 2, k));
+    return v;
+}
+
+// Power-of-two boundary factor of 1/cell_volume: 1/(h_x h_y h_z) * 2^(#end axes),
+// which is exact because halving is exact.
+__device__ __forceinline__ double inv_volume_fast(const Geo& g, double inv_base, int i, int j, int k) {
+    int e = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
+    if (g.dim == 3) e += (k == 0 || k == g.nz - 1);
+    return inv_base * (double)(1 << e);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum in a fixed order (warp butterflies, then warp 0 over the warp
+// partials): deterministic for a fixed launch shape.  Result valid in thread 0.
+template <int NWARPS>
+__device__ double block_sum(double v, double* scratch) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = l < NWARPS ? scratch[l] : 0.0;
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+// ----------------------------------------------------------- mbarrier / TMA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+        "%6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+}  // namespace petto_b200

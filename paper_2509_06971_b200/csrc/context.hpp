@@ -1,0 +1,83 @@
+// context.hpp -- the device context behind the petto_dev_* C-ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/petto_dev.h"
+#include "common.cuh"
+
+namespace petto_b200 {
+
+
+}  // namespace petto_b200
+
+struct petto_ctx {
+    petto_grid_desc desc{};
+    petto_b200::Geo g{};
+    int comps = 1;
+    int mode = PETTO_MODE_FAST;
+    int device = 0;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // fields (device, pitched layout)
+    double* st[3] = {nullptr, nullptr, nullptr};
+    int cur = 0, prev = 1;
+    double* prop = nullptr;        // kappa or Young's modulus
+    double* src = nullptr;         // dense source/loads (replica path, heat dense)
+    bool src_uniform = true;
+    double src_value = 0.0;
+    double* aux = nullptr;         // pinned values at constrained entries, loads elsewhere
+    unsigned char* mask = nullptr; // bit c pinned, bit 3 load
+    long long* cons_ent = nullptr; // device-local constrained entries (owned planes)
+    double* cons_val = nullptr;
+    long long ncons = 0;
+    double* r = nullptr;           // residual scratch
+    double* Kdev = nullptr;        // unit-cell stiffness (replica)
+    std::vector<double> K, kh;
+    double nu_op = 0.3;
+    bool op_ready = false;
+    bool state_set = false;
+
+    double prop_node0 = 0.0;       // property at global node 0 (operator nu, :299-301)
+    bool prop_node0_valid = false;
+
+    double* partials = nullptr;
+    int npartials = 0;
+    int npartials_used = 0;
+    petto_b200::DeviceStatus* status = nullptr;  // device
+    petto_b200::DeviceStatus* status_h = nullptr; // pinned host mirror
+
+    // TMA descriptors for the fused 3D kernel
+    CUtensorMap tU[3], tP[3], tE, tM;
+    bool tmaps = false;
+
+    // design subsystem
+    petto_material mat{};
+    petto_targets tgt{};
+    petto_weights wts{};
+    std::vector<int64_t> region_nodes;
+    bool design_set = false;
+    double* phases = nullptr;      // P x Ns
+    double* gc = nullptr;          // P x Ns compliance sensitivity
+    double* scratch1 = nullptr;    // Ns
+    double* scratch2 = nullptr;    // Ns
+    long long* region_dev = nullptr;
+    double* dscal = nullptr;       // device scalars for the design kernels
+
+    // instrumentation
+    long long launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    int ev_used = 0;
+    double kernel_ms = 0.0;
+    long long kernel_launches = 0;
+    double bytes_per_launch = 0.0;
+    std::string kernel_name;
+};

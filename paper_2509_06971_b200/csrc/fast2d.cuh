@@ -1,0 +1,159 @@
+// fast2d.cuh -- fused residual + PT/APT update kernels for the small operators:
+// heat conduction (2D/3D, HeatOperator::residual -> variable_diffusion_into,
+// stencil.hpp:123-158) and 2D plane-strain elasticity (modal form, 10 nonzeros).
+// One thread per owned node; neighbours come through L1/L2 (the C1-C3 working
+// sets are L2-resident, so these are latency/launch-bound rather than HBM-bound).
+#pragma once
+
+#include "common.cuh"
+
+namespace petto_b200 {
+
+struct FusedParams {
+    Geo g;
+    int form;           // 0 APT explicit, 1 APT semi-implicit, 2 PT, 3 residual only
+    double dt, a, b, inv;
+    const double* cur;
+    const double* prev;
+    double* next;       // may alias prev
+    const double* prop; // kappa (heat) / Young's modulus E (elasticity)
+    const unsigned char* mask;  // bit c: component c pinned; bit 3: load present
+    const double* aux;  // pinned values / loads
+    const double* src;  // heat: dense source (nullable -> src_uniform)
+    double src_uniform;
+    double kh[10];      // 2D modal stiffness
+    double e_scale;     // sum of 4 corner E -> E_cell
+    double inv_base;    // 1/(hx hy [hz])
+    double* partials;   // per-block r^2 (nullable)
+    DeviceStatus* status;
+    long long step, nsteps;
+};
+
+__device__ __forceinline__ double fused_update(const FusedParams& P, double r, double cu, long long e, int c,
+                                               unsigned char mk, double& rsq) {
+    if ((mk >> c) & 1) return P.form == 3 ? 0.0 : P.aux[e];
+    rsq += r * r;
+    switch (P.form) {
+        case 0: {
+            const double pp = P.prev[e];
+            return 2.0 * cu - pp + P.a * r - P.b * (cu - pp);
+        }
+        case 1: {
+            const double pp = P.prev[e];
+            return (2.0 * cu - pp + P.b * cu + P.a * r) * P.inv;
+        }
+        case 2:
+            return cu + P.dt * r;
+        default:
+            return r;
+    }
+}
+
+__device__ __forceinline__ double flux_fast(const double* f, const double* kp, int t, int n, long long s,
+                                            double hih2) {
+    if (n == 1) return 0.0;
+    const double f0 = f[0], k0 = kp[0];
+    if (t == 0) return (k0 + kp[s]) * (f[s] - f0) * (2.0 * hih2);
+    if (t == n - 1) return (k0 + kp[-s]) * (f[-s] - f0) * (2.0 * hih2);
+    return ((k0 + kp[s]) * (f[s] - f0) - (kp[-s] + k0) * (f0 - f[-s])) * hih2;
+}
+
+template <int NT>
+__device__ __forceinline__ void finish_block(const FusedParams& P, double rsq, unsigned bad) {
+    __shared__ double scratch[32];
+    const double s = block_sum<NT / 32>(rsq, scratch);
+    if (threadIdx.x == 0 && P.partials) P.partials[blockIdx.x] = s;
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) {
+        if (bad & 2u) atomicOr(&P.status->flags, 2u);
+        if (bad & 1u) mark_bad(P.status, P.step);
+    }
+}
+
+// Heat: grid-stride over owned nodes (fixed grid => deterministic partials).
+__global__ void __launch_bounds__(256) k_heat_fast(const FusedParams P) {
+    const Geo& g = P.g;
+    if (skip_step(P.status, P.step, P.nsteps)) return;
+    const long long plane = (long long)g.nx * g.ny;
+    const long long owned = plane * (g.ke - g.kb);
+    double hih2[3];
+    for (int a = 0; a < 3; ++a) hih2[a] = 0.5 / (g.h[a] * g.h[a]);
+    double rsq = 0.0;
+    unsigned bad = 0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int k = g.kb + (int)(t / plane);
+        const long long rr = t - (long long)(k - g.kb) * plane;
+        const int j = (int)(rr / g.nx);
+        const int i = (int)(rr - (long long)j * g.nx);
+        const long long node = lidx(g, i, j, k);
+        const double* T = P.cur + node;
+        const double* kp = P.prop + node;
+        if (!(kp[0] > 0.0)) bad |= 2u;
+        double acc = flux_fast(T, kp, i, g.nx, 1, hih2[0]) + flux_fast(T, kp, j, g.ny, g.px, hih2[1]);
+        if (g.nz > 1) acc += flux_fast(T, kp, k, g.nz, (long long)g.px * g.ny, hih2[2]);
+        const double r = acc + (P.src ? P.src[node] : P.src_uniform);
+        const double nv = fused_update(P, r, T[0], node, 0, P.mask[node], rsq);
+        bad |= !isfinite(nv);
+        P.next[node] = nv;
+    }
+    finish_block<256>(P, rsq, bad);
+}
+
+// 2D plane-strain elasticity: each node gathers the corner forces of its (up to)
+// four cells, evaluated in the modal basis (stiffness.hpp pattern order).
+__global__ void __launch_bounds__(256) k_elastic2d_fast(const FusedParams P) {
+    const Geo& g = P.g;
+    if (skip_step(P.status, P.step, P.nsteps)) return;
+    const long long owned = (long long)g.nx * g.ny;
+    const double* k = P.kh;
+    double rsq = 0.0;
+    unsigned bad = 0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(t / g.nx);
+        const int i = (int)(t - (long long)j * g.nx);
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {  // this node is corner m of cell (i - bx, j - by)
+            const int ci = i - (m & 1), cj = j - (m >> 1);
+            if (ci < 0 || ci > g.nx - 2 || cj < 0 || cj > g.ny - 2) continue;
+            const long long b = lidx(g, ci, cj, 0);
+            const long long o[4] = {b, b + 1, b + g.px, b + g.px + 1};
+            double C[4][2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const double* u = P.cur + c * g.Ns;
+                const double v0 = u[o[0]], v1 = u[o[1]], v2 = u[o[2]], v3 = u[o[3]];
+                C[1][c] = (v0 - v1) + (v2 - v3);
+                C[2][c] = (v0 + v1) - (v2 + v3);
+                C[3][c] = (v0 - v1) - (v2 - v3);
+            }
+            const double ec = ((P.prop[o[0]] + P.prop[o[1]]) + (P.prop[o[2]] + P.prop[o[3]])) * P.e_scale;
+            const double F10 = ec * (k[0] * C[1][0] + k[1] * C[2][1]);
+            const double F11 = ec * (k[2] * C[1][1] + k[3] * C[2][0]);
+            const double F20 = ec * (k[4] * C[1][1] + k[5] * C[2][0]);
+            const double F21 = ec * (k[6] * C[1][0] + k[7] * C[2][1]);
+            const double F30 = ec * (k[8] * C[3][0]);
+            const double F31 = ec * (k[9] * C[3][1]);
+            const double s1 = (m & 1) ? -1.0 : 1.0, s2 = (m & 2) ? -1.0 : 1.0, s3 = s1 * s2;
+            acc[0] += s1 * F10 + s2 * F20 + s3 * F30;
+            acc[1] += s1 * F11 + s2 * F21 + s3 * F31;
+        }
+        const long long node = lidx(g, i, j, 0);
+        const double invv = inv_volume_fast(g, P.inv_base, i, j, 0);
+        const unsigned char mk = P.mask[node];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const long long e = c * g.Ns + node;
+            const double f = ((mk & 8) && !((mk >> c) & 1)) ? P.aux[e] : 0.0;
+            const double r = -acc[c] * invv - f;
+            const double nv = fused_update(P, r, P.cur[e], e, c, mk, rsq);
+            bad |= !isfinite(nv);
+            P.next[e] = nv;
+        }
+    }
+    finish_block<256>(P, rsq, bad);
+}
+
+}  // namespace petto_b200

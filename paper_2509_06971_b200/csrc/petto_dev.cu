@@ -1,0 +1,874 @@
+// petto_dev.cu -- C-ABI implementation: device context, uploads, and the state
+// solver (hybrid_solve / iterate_to_tolerance / residual) on B200.
+//
+// Reference seam: include/petto/state_solver.hpp (StateOperator, hybrid_solve,
+// iterate_to_tolerance).  Every step loop runs without host synchronisation:
+// non-finite detection and the tolerance test are evaluated by the kernels
+// themselves through the context's DeviceStatus block.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "context.hpp"
+#include "design.cuh"
+#include "elastic3d.cuh"
+#include "fast2d.cuh"
+#include "replica.cuh"
+#include "stiffness.hpp"
+
+using namespace petto_b200;
+
+namespace {
+
+thread_local std::string g_err;  // errors before a context exists
+
+int fail(petto_ctx* ctx, int code, const std::string& msg) {
+    (ctx ? ctx->err : g_err) = msg;
+    return code;
+}
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+long long global_nodes(const petto_ctx* ctx) {
+    return (long long)ctx->g.nx * ctx->g.ny * ctx->g.nz;
+}
+
+long long owned_nodes(const petto_ctx* ctx) {
+    return (long long)ctx->g.nx * ctx->g.ny * (ctx->g.ke - ctx->g.kb);
+}
+
+int blocks_for(long long n, int threads = 256) { return (int)std::max(1LL, (n + threads - 1) / threads); }
+
+// Host (global, dense) <-> device (local, pitched) copies of `comps` components.
+int upload(petto_ctx* ctx, double* dst, const double* host, int comps) {
+    const Geo& g = ctx->g;
+    const long long N = global_nodes(ctx);
+    for (int c = 0; c < comps; ++c)
+        CK(cudaMemcpy2DAsync(dst + c * g.Ns, (size_t)g.px * 8, host + c * N + (long long)g.ks0 * g.nx * g.ny,
+                             (size_t)g.nx * 8, (size_t)g.nx * 8, (size_t)g.ny * g.nzs, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    return PETTO_OK;
+}
+
+int download(petto_ctx* ctx, double* host, const double* src, int comps) {
+    const Geo& g = ctx->g;
+    const long long N = global_nodes(ctx);
+    for (int c = 0; c < comps; ++c)
+        CK(cudaMemcpy2DAsync(host + c * N + (long long)g.kb * g.nx * g.ny, (size_t)g.nx * 8,
+                             src + c * g.Ns + lidx(g, 0, 0, g.kb), (size_t)g.px * 8, (size_t)g.nx * 8,
+                             (size_t)g.ny * (g.ke - g.kb), cudaMemcpyDeviceToHost, ctx->stream));
+    return PETTO_OK;
+}
+
+// Global entry comp*N + node -> local entry comp*Ns + lidx, or -1 if the node is
+// not on an owned plane of this rank.
+long long local_entry(const petto_ctx* ctx, long long e, int* comp = nullptr, long long* node_out = nullptr) {
+    const Geo& g = ctx->g;
+    const long long N = global_nodes(ctx);
+    const int c = (int)(e / N);
+    const long long node = e - (long long)c * N;
+    const long long plane = (long long)g.nx * g.ny;
+    const int k = (int)(node / plane);
+    const long long r = node - (long long)k * plane;
+    const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
+    if (k < g.kb || k >= g.ke) return -1;
+    if (comp) *comp = c;
+    if (node_out) *node_out = lidx(g, i, j, k);
+    return c * g.Ns + lidx(g, i, j, k);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+int make_tmaps(petto_ctx* ctx) {
+    const Geo& g = ctx->g;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return fail(ctx, PETTO_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t d4[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs, 3};
+    const cuuint64_t s4[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8, (cuuint64_t)g.Ns * 8};
+    const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, 1, 3};
+    const cuuint32_t boxP[4] = {32, e3::W, 1, 3};
+    const cuuint32_t one[4] = {1, 1, 1, 1};
+    for (int b = 0; b < 3; ++b) {
+        if (enc(&ctx->tU[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxU, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(ctx, PETTO_ERROR, "tensor map (state) encode failed");
+        if (enc(&ctx->tP[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxP, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(ctx, PETTO_ERROR, "tensor map (previous) encode failed");
+    }
+    const cuuint64_t d3[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs};
+    const cuuint64_t s3[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8};
+    const cuuint32_t boxE[3] = {e3::BOXX, e3::UROWS, 1};
+    if (enc(&ctx->tE, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->prop, d3, s3, boxE, one,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(ctx, PETTO_ERROR, "tensor map (modulus) encode failed");
+    const cuuint64_t sm[2] = {(cuuint64_t)g.px, (cuuint64_t)g.px * g.ny};
+    const cuuint32_t boxM[3] = {32, e3::W, 1};
+    if (enc(&ctx->tM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->mask, d3, sm, boxM, one,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(ctx, PETTO_ERROR, "tensor map (mask) encode failed");
+    ctx->tmaps = true;
+    return PETTO_OK;
+}
+
+// ------------------------------------------------------------------- kernels
+
+__global__ void k_scatter_bytes(const long long* __restrict__ idx, const unsigned char* __restrict__ v, long long n,
+                                unsigned char* out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[idx[t]] = v[t];
+}
+
+__global__ void k_scatter_values(const long long* __restrict__ idx, const double* __restrict__ v, long long n,
+                                 double* out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[idx[t]] = v[t];
+}
+
+// Lame positivity check of the ElasticityOperator constructor
+// (state_solver.hpp:295-297) and kappa > 0 of variable_diffusion (stencil.hpp:145).
+__global__ void k_check_positive(Geo g, const double* __restrict__ p, double c1, double c2, unsigned* flag) {
+    int i, j, k;
+    if (!owned_node(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, i, j, k)) return;
+    const double v = p[lidx(g, i, j, k)];
+    if (!(c1 * v > 0.0) || !(c2 * v > 0.0)) atomicOr(flag, 1u);
+}
+
+// iterate_to_tolerance bookkeeping after residual #iter (state_solver.hpp:517-539):
+// r = sqrt(sum r^2)/N; record, test, and raise the stop flag on the device.
+__global__ void k_iter_finish(DeviceStatus* s, const double* __restrict__ partials, int n) {
+    __shared__ double scratch[32];
+    if (s->done) return;
+    double v = 0.0;
+    if (partials)
+        for (int t = threadIdx.x; t < n; t += blockDim.x) v += partials[t];
+    const double tot = block_sum<8>(v, scratch);
+    if (threadIdx.x != 0) return;
+    const double sq = partials ? tot : s->sumsq;
+    const double r = sqrt(sq) / s->nodes;
+    const long long k = s->iter;
+    if (k == 0) {
+        s->r_initial = r;
+        s->r_final = r;
+        if (r < s->target) {
+            s->done = 1;
+            s->converged = 1;
+        } else if (s->max_iters <= 0) {
+            s->done = 1;
+        }
+    } else {
+        s->iterations = k;
+        s->r_final = r;
+        if (!isfinite(r)) {
+            s->done = 1;
+            s->aborted = 1;
+        } else if (r < s->target) {
+            s->done = 1;
+            s->converged = 1;
+        } else if (k >= s->max_iters) {
+            s->done = 1;
+        }
+    }
+    s->iter = k + 1;
+}
+
+__global__ void k_sum_to(const double* __restrict__ partials, int n, double* out) {
+    __shared__ double scratch[32];
+    double v = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) v += partials[t];
+    const double tot = block_sum<8>(v, scratch);
+    if (threadIdx.x == 0) *out = tot;
+}
+
+// ------------------------------------------------------------- state launches
+
+struct StepCoef {
+    int form;  // 0 APT explicit, 1 APT semi, 2 PT, 3 residual
+    double dt, a, b, inv;
+};
+
+StepCoef coef(int form, double dt, double theta) {
+    StepCoef c{form, dt, 0.0, 0.0, 1.0};
+    if (form <= 1) {  // apt_step_inplace (state_solver.hpp:423-435)
+        c.a = dt * dt / theta;
+        c.b = dt / theta;
+        c.inv = 1.0 / (1.0 + c.b);
+    }
+    return c;
+}
+
+int fast_grid_3d(const petto_ctx* ctx, long long units) {
+    // persistent CTAs (one per SM), but keep z sub-runs >= 8 planes long
+    long long want = std::max(1LL, units / 8);
+    return (int)std::min<long long>(ctx->nsm, want);
+}
+
+void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
+    if (!ctx->timing) return;
+    if (ctx->ev_used + 2 > (int)ctx->ev_pool.size()) {
+        // drain the pool
+        cudaStreamSynchronize(ctx->stream);
+        for (int e = 0; e + 1 < ctx->ev_used; e += 2) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]);
+            ctx->kernel_ms += ms;
+        }
+        ctx->ev_used = 0;
+    }
+    ev[0] = ctx->ev_pool[ctx->ev_used];
+    ev[1] = ctx->ev_pool[ctx->ev_used + 1];
+    ctx->ev_used += 2;
+    cudaEventRecord(ev[0], ctx->stream);
+}
+
+void timing_end(petto_ctx* ctx, cudaEvent_t* ev, const char* name, double bytes) {
+    if (!ctx->timing) return;
+    cudaEventRecord(ev[1], ctx->stream);
+    ctx->kernel_launches += 1;
+    ctx->bytes_per_launch = bytes;
+    ctx->kernel_name = name;
+}
+
+// One fused (fast) or replica state step: reads st[cur] (and st[prev]), writes
+// `next` (a state buffer or the residual scratch for form 3).
+int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, long long step, long long nsteps,
+               bool want_partials) {
+    const Geo& g = ctx->g;
+    double* partials = want_partials ? ctx->partials : nullptr;
+    if (ctx->mode == PETTO_MODE_FAST) {
+        cudaEvent_t ev[2];
+        const long long owned = owned_nodes(ctx);
+        if (g.dim == 3 && ctx->desc.physics == 1) {
+            if (!ctx->tmaps && make_tmaps(ctx)) return PETTO_ERROR;
+            e3::Params P{};
+            P.g = g;
+            for (int i = 0; i < 45; ++i) P.kh[i] = ctx->kh[i];
+            const double nu = ctx->desc.poisson_ratio;
+            P.e_scale = (1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
+            P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
+            P.form = k.form;
+            P.dt = k.dt;
+            P.a = k.a;
+            P.b = k.b;
+            P.inv = k.inv;
+            P.next = next;
+            P.aux = ctx->aux;
+            P.partials = partials;
+            P.status = ctx->status;
+            P.step = step;
+            P.nsteps = nsteps;
+            P.ntx = (g.nx + 31) / 32;
+            P.nzo = g.ke - g.kb;
+            const int nstrips = (g.ny + e3::W - 1) / e3::W;
+            P.units = (long long)nstrips * P.nzo;
+            const int grid = fast_grid_3d(ctx, P.units);
+            if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
+            timing_begin(ctx, ev);
+            e3::k_elastic3d_fast<<<grid, e3::NTHREADS, e3::SMEM_BYTES, ctx->stream>>>(
+                P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM);
+            timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
+            ctx->launches++;
+            CKL();
+            if (partials) ctx->npartials_used = grid;
+            return PETTO_OK;
+        }
+        FusedParams P{};
+        P.g = g;
+        P.form = k.form;
+        P.dt = k.dt;
+        P.a = k.a;
+        P.b = k.b;
+        P.inv = k.inv;
+        P.cur = ctx->st[cur];
+        P.prev = ctx->st[prev];
+        P.next = next;
+        P.prop = ctx->prop;
+        P.mask = ctx->mask;
+        P.aux = ctx->aux;
+        P.src = ctx->src_uniform ? nullptr : ctx->src;
+        P.src_uniform = ctx->src_value;
+        for (int i = 0; i < 10 && i < (int)ctx->kh.size(); ++i) P.kh[i] = ctx->kh[i];
+        const double nu = ctx->desc.poisson_ratio;
+        P.e_scale = (1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 4.0);
+        P.inv_base = g.dim == 3 ? 1.0 / (g.h[0] * g.h[1] * g.h[2]) : 1.0 / (g.h[0] * g.h[1]);
+        P.partials = partials;
+        P.status = ctx->status;
+        P.step = step;
+        P.nsteps = nsteps;
+        const int grid = (int)std::min<long long>(ctx->npartials, blocks_for(owned));
+        timing_begin(ctx, ev);
+        if (ctx->desc.physics == 0) {
+            k_heat_fast<<<grid, 256, 0, ctx->stream>>>(P);
+            timing_end(ctx, ev, "k_heat_fast", (double)owned * (k.form <= 1 ? 33.0 : 25.0));
+        } else {
+            k_elastic2d_fast<<<grid, 256, 0, ctx->stream>>>(P);
+            timing_end(ctx, ev, "k_elastic2d_fast", (double)owned * (k.form <= 1 ? 57.0 : 41.0));
+        }
+        ctx->launches++;
+        CKL();
+        if (partials) ctx->npartials_used = grid;
+        return PETTO_OK;
+    }
+    // replica: residual, [zero constrained], update, apply constraints
+    const long long owned = owned_nodes(ctx);
+    const int nb = blocks_for(owned);
+    double* r = k.form == 3 ? next : ctx->r;
+    if (ctx->desc.physics == 1) {
+        const double cm = 1.0 / (2.0 * (1.0 + ctx->desc.poisson_ratio));
+        k_elastic_residual_replica<<<nb, 256, 0, ctx->stream>>>(g, ctx->st[cur], ctx->prop, cm, ctx->src,
+                                                                ctx->Kdev, 2.0 * (1.0 + ctx->nu_op) / (1 << g.dim),
+                                                                r, ctx->status, step, nsteps);
+    } else {
+        k_heat_residual_replica<<<nb, 256, 0, ctx->stream>>>(g, ctx->st[cur], ctx->prop, ctx->src, ctx->src_value,
+                                                             ctx->src_uniform ? 0 : 1, r, ctx->status, step,
+                                                             nsteps);
+    }
+    ctx->launches++;
+    CKL();
+    if (k.form == 3) {
+        if (ctx->ncons) {
+            k_zero_entries<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->ncons, r,
+                                                                           ctx->status, step, nsteps);
+            ctx->launches++;
+        }
+        if (want_partials) {
+            k_sumsq_serial<<<1, 32, 0, ctx->stream>>>(g, ctx->comps, r, &ctx->status->sumsq);
+            ctx->launches++;
+        }
+        CKL();
+        return PETTO_OK;
+    }
+    k_update_replica<<<nb, 256, 0, ctx->stream>>>(g, ctx->comps, k.form, ctx->st[cur], ctx->st[prev], r, next, k.dt,
+                                                  k.a, k.b, k.inv, ctx->status, step, nsteps);
+    ctx->launches++;
+    if (ctx->ncons) {
+        k_apply_constraints<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->cons_val,
+                                                                             ctx->ncons, next, ctx->status, step,
+                                                                             nsteps);
+        ctx->launches++;
+    }
+    CKL();
+    return PETTO_OK;
+}
+
+int reset_status(petto_ctx* ctx) {
+    DeviceStatus s{};
+    s.first_bad = PETTO_NO_BAD;
+    s.nodes = (double)global_nodes(ctx);
+    *ctx->status_h = s;
+    CK(cudaMemcpyAsync(ctx->status, ctx->status_h, sizeof(DeviceStatus), cudaMemcpyHostToDevice, ctx->stream));
+    return PETTO_OK;
+}
+
+int read_status(petto_ctx* ctx) {
+    CK(cudaMemcpyAsync(ctx->status_h, ctx->status, sizeof(DeviceStatus), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int require_ready(petto_ctx* ctx) {
+    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
+    if (ctx->desc.physics == 1 && !ctx->op_ready)
+        return fail(ctx, PETTO_INVALID, "elasticity operator not initialised (petto_dev_init_operator)");
+    return PETTO_OK;
+}
+
+// kappa > 0 guard of variable_diffusion_into (stencil.hpp:145-157), checked once per
+// call because kappa is constant within a solve.
+int check_kappa(petto_ctx* ctx) {
+    if (ctx->desc.physics != 0) return PETTO_OK;
+    CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
+    k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->prop, 1.0, 1.0,
+                                                                            &ctx->status->flags);
+    ctx->launches++;
+    CKL();
+    if (int rc = read_status(ctx)) return rc;
+    if (ctx->status_h->flags & 1u)
+        return fail(ctx, PETTO_INVALID, "variable_diffusion: kappa must be positive everywhere");
+    return PETTO_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+
+extern "C" {
+
+const char* petto_dev_version(void) { return "petto_b200 0.1 (sm_100a)"; }
+
+int petto_dev_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+const char* petto_dev_last_error(const petto_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+void* petto_dev_stream(petto_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
+    petto_ctx* ctx = nullptr;
+    *out = nullptr;
+    if (d->dim != 2 && d->dim != 3) return fail(nullptr, PETTO_INVALID, "grid: dim must be 2 or 3");
+    for (int a = 0; a < d->dim; ++a) {
+        if (d->n[a] < 3) return fail(nullptr, PETTO_INVALID, "grid: need at least 3 nodes per axis");
+        if (!(d->length[a] > 0.0)) return fail(nullptr, PETTO_INVALID, "grid: axis length must be positive");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= d->device)
+        return fail(nullptr, PETTO_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, d->device) != cudaSuccess || prop.major < 10)
+        return fail(nullptr, PETTO_ERROR, "device is not sm_100-class (Blackwell) -- no fallback");
+    if (cudaSetDevice(d->device) != cudaSuccess) return fail(nullptr, PETTO_ERROR, "cudaSetDevice failed");
+
+    ctx = new petto_ctx();
+    ctx->desc = *d;
+    ctx->device = d->device;
+    ctx->nsm = prop.multiProcessorCount;
+    ctx->mode = d->mode;
+    ctx->comps = d->physics ? d->dim : 1;
+    Geo& g = ctx->g;
+    g.dim = d->dim;
+    g.nx = (int)d->n[0];
+    g.ny = (int)d->n[1];
+    g.nz = d->dim == 3 ? (int)d->n[2] : 1;
+    for (int a = 0; a < 3; ++a) g.h[a] = 1.0;
+    for (int a = 0; a < d->dim; ++a) g.h[a] = d->length[a] / (double)(d->n[a] - 1);
+    g.kb = (int)(d->k_end > d->k_begin ? d->k_begin : 0);
+    g.ke = (int)(d->k_end > d->k_begin ? d->k_end : g.nz);
+    if (g.kb < 0 || g.ke > g.nz || g.kb >= g.ke) {
+        delete ctx;
+        return fail(nullptr, PETTO_INVALID, "slab: need 0 <= k_begin < k_end <= nz");
+    }
+    g.ks0 = std::max(0, g.kb - 1);
+    g.nzs = std::min(g.nz, g.ke + 1) - g.ks0;
+    g.px = (g.nx + 15) / 16 * 16;
+    g.Ns = (long long)g.px * g.ny * g.nzs;
+
+    auto cleanup = [&](const std::string& m) {
+        petto_dev_destroy(ctx);
+        return fail(nullptr, PETTO_ERROR, m);
+    };
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup("stream creation failed");
+    const size_t fb = sizeof(double) * (size_t)g.Ns;
+    for (int b = 0; b < 3; ++b)
+        if (cudaMalloc(&ctx->st[b], fb * ctx->comps) != cudaSuccess) return cleanup("out of device memory (state)");
+    if (cudaMalloc(&ctx->prop, fb) != cudaSuccess || cudaMalloc(&ctx->aux, fb * ctx->comps) != cudaSuccess ||
+        cudaMalloc(&ctx->mask, (size_t)g.Ns) != cudaSuccess || cudaMalloc(&ctx->src, fb * ctx->comps) != cudaSuccess ||
+        cudaMalloc(&ctx->r, fb * ctx->comps) != cudaSuccess)
+        return cleanup("out of device memory (fields)");
+    for (int b = 0; b < 3; ++b) cudaMemsetAsync(ctx->st[b], 0, fb * ctx->comps, ctx->stream);
+    cudaMemsetAsync(ctx->prop, 0, fb, ctx->stream);
+    cudaMemsetAsync(ctx->aux, 0, fb * ctx->comps, ctx->stream);
+    cudaMemsetAsync(ctx->mask, 0, (size_t)g.Ns, ctx->stream);
+    cudaMemsetAsync(ctx->src, 0, fb * ctx->comps, ctx->stream);
+    cudaMemsetAsync(ctx->r, 0, fb * ctx->comps, ctx->stream);
+    ctx->npartials = std::max(4 * ctx->nsm, 1024);
+    if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
+        cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
+        cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
+        cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess)
+        return cleanup("out of device memory (scalars)");
+    if (cudaFuncSetAttribute(e3::k_elastic3d_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, e3::SMEM_BYTES) !=
+        cudaSuccess)
+        return cleanup("cannot configure shared memory for k_elastic3d_fast");
+    if (reset_status(ctx)) return cleanup(ctx->err);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");
+    *out = ctx;
+    return PETTO_OK;
+}
+
+void petto_dev_destroy(petto_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
+    cudaFree(ctx->prop);
+    cudaFree(ctx->aux);
+    cudaFree(ctx->mask);
+    cudaFree(ctx->src);
+    cudaFree(ctx->r);
+    cudaFree(ctx->cons_ent);
+    cudaFree(ctx->cons_val);
+    cudaFree(ctx->Kdev);
+    cudaFree(ctx->partials);
+    cudaFree(ctx->status);
+    cudaFree(ctx->dscal);
+    if (ctx->status_h) cudaFreeHost(ctx->status_h);
+    design_free(ctx);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int petto_dev_set_mode(petto_ctx* ctx, int mode) {
+    if (mode != PETTO_MODE_FAST && mode != PETTO_MODE_REPLICA) return fail(ctx, PETTO_INVALID, "unknown mode");
+    ctx->mode = mode;
+    return PETTO_OK;
+}
+
+int petto_dev_set_constraints(petto_ctx* ctx, const int64_t* entry, const double* value, int64_t count) {
+    CK(cudaSetDevice(ctx->device));
+    const Geo& g = ctx->g;
+    std::vector<long long> ent;
+    std::vector<double> val;
+    std::unordered_map<long long, unsigned char> bits;
+    for (int64_t t = 0; t < count; ++t) {
+        int c = 0;
+        long long node = 0;
+        const long long le = local_entry(ctx, entry[t], &c, &node);
+        if (entry[t] < 0 || entry[t] >= global_nodes(ctx) * ctx->comps)
+            return fail(ctx, PETTO_INVALID, "constraint entry outside the field");
+        if (le < 0) continue;
+        ent.push_back(le);
+        val.push_back(value[t]);
+        bits[node] |= (unsigned char)(1u << c);
+    }
+    cudaFree(ctx->cons_ent);
+    cudaFree(ctx->cons_val);
+    ctx->cons_ent = nullptr;
+    ctx->cons_val = nullptr;
+    ctx->ncons = (long long)ent.size();
+    if (ctx->ncons) {
+        CK(cudaMalloc(&ctx->cons_ent, sizeof(long long) * ent.size()));
+        CK(cudaMalloc(&ctx->cons_val, sizeof(double) * val.size()));
+        CK(cudaMemcpyAsync(ctx->cons_ent, ent.data(), sizeof(long long) * ent.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->cons_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+    }
+    // mask bits 0-2 from the constraints; bit 3 (load) is preserved from set_source
+    std::vector<unsigned char> hmask;
+    hmask.resize((size_t)g.Ns);
+    CK(cudaMemcpyAsync(hmask.data(), ctx->mask, (size_t)g.Ns, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto& b : hmask) b &= 8u;
+    for (const auto& kv : bits) hmask[kv.first] |= kv.second;
+    CK(cudaMemcpyAsync(ctx->mask, hmask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
+    // pinned values into aux
+    if (ctx->ncons)
+        k_scatter_values<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->cons_val, ctx->ncons,
+                                                                          ctx->aux);
+    ctx->launches++;
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int petto_dev_set_source(petto_ctx* ctx, const double* source) {
+    CK(cudaSetDevice(ctx->device));
+    const Geo& g = ctx->g;
+    const long long N = global_nodes(ctx);
+    if (int rc = upload(ctx, ctx->src, source, ctx->comps)) return rc;
+    if (ctx->desc.physics == 0) {
+        // uniform source: the fused kernel reads a scalar instead of a field
+        bool uni = true;
+        for (long long n = (long long)g.kb * g.nx * g.ny; n < (long long)g.ke * g.nx * g.ny && uni; ++n)
+            uni = source[n] == source[(long long)g.kb * g.nx * g.ny];
+        ctx->src_uniform = uni;
+        ctx->src_value = source[(long long)g.kb * g.nx * g.ny];
+        CK(cudaStreamSynchronize(ctx->stream));
+        return PETTO_OK;
+    }
+    // elasticity: sparse loads -> aux at unpinned entries, mask bit 3
+    std::vector<unsigned char> hmask((size_t)g.Ns);
+    CK(cudaMemcpyAsync(hmask.data(), ctx->mask, (size_t)g.Ns, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<long long> idx;
+    std::vector<double> val;
+    for (auto& b : hmask) b &= 7u;
+    for (int c = 0; c < ctx->comps; ++c)
+        for (long long n = (long long)g.kb * g.nx * g.ny; n < (long long)g.ke * g.nx * g.ny; ++n) {
+            const double v = source[c * N + n];
+            if (v == 0.0) continue;
+            long long node = 0;
+            int cc = 0;
+            const long long le = local_entry(ctx, c * N + n, &cc, &node);
+            if (le < 0) continue;
+            if (!((hmask[node] >> c) & 1)) {
+                idx.push_back(le);
+                val.push_back(v);
+            }
+            hmask[node] |= 8u;
+        }
+    // clear stale loads (keep pinned values), then scatter
+    std::vector<long long> pins;
+    // aux := 0 except pinned entries
+    CK(cudaMemsetAsync(ctx->aux, 0, sizeof(double) * (size_t)g.Ns * ctx->comps, ctx->stream));
+    if (ctx->ncons)
+        k_scatter_values<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->cons_val, ctx->ncons,
+                                                                          ctx->aux);
+    if (!idx.empty()) {
+        long long* di = nullptr;
+        double* dv = nullptr;
+        CK(cudaMalloc(&di, sizeof(long long) * idx.size()));
+        CK(cudaMalloc(&dv, sizeof(double) * val.size()));
+        CK(cudaMemcpyAsync(di, idx.data(), sizeof(long long) * idx.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dv, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice, ctx->stream));
+        k_scatter_values<<<blocks_for((long long)idx.size()), 256, 0, ctx->stream>>>(di, dv, (long long)idx.size(),
+                                                                                     ctx->aux);
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(di);
+        cudaFree(dv);
+    }
+    CK(cudaMemcpyAsync(ctx->mask, hmask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int petto_dev_set_property(petto_ctx* ctx, const double* property) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = upload(ctx, ctx->prop, property, 1)) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->prop_node0 = property[0];
+    ctx->prop_node0_valid = true;
+    return PETTO_OK;
+}
+
+int petto_dev_init_operator(petto_ctx* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->desc.physics == 0) {
+        ctx->op_ready = true;
+        return PETTO_OK;
+    }
+    const double nu = ctx->desc.poisson_ratio;
+    const double cl = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double cm = 1.0 / (2.0 * (1.0 + nu));
+    CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
+    k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->prop, cl, cm,
+                                                                            &ctx->status->flags);
+    ctx->launches++;
+    CKL();
+    if (int rc = read_status(ctx)) return rc;
+    if (ctx->status_h->flags & 1u) return fail(ctx, PETTO_INVALID, "elasticity: Lame fields must be positive");
+    // nu from node 0's Lame pair (state_solver.hpp:299-301)
+    double e0 = ctx->prop_node0;
+    if (!ctx->prop_node0_valid) {
+        if (ctx->g.kb != 0) return fail(ctx, PETTO_INVALID, "node 0 property unknown on this rank");
+        CK(cudaMemcpy(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    const double l0 = cl * e0, m0 = cm * e0;
+    ctx->nu_op = l0 / (2.0 * (l0 + m0));
+    ctx->K = unit_cell_stiffness(ctx->g.dim, ctx->g.h, ctx->nu_op);
+    try {
+        ctx->kh = modal_stiffness(ctx->g.dim, ctx->K);
+    } catch (const std::exception& e) {
+        return fail(ctx, PETTO_ERROR, e.what());
+    }
+    cudaFree(ctx->Kdev);
+    CK(cudaMalloc(&ctx->Kdev, sizeof(double) * ctx->K.size()));
+    CK(cudaMemcpy(ctx->Kdev, ctx->K.data(), sizeof(double) * ctx->K.size(), cudaMemcpyHostToDevice));
+    ctx->op_ready = true;
+    return PETTO_OK;
+}
+
+int petto_dev_set_state(petto_ctx* ctx, const double* current, const double* previous) {
+    CK(cudaSetDevice(ctx->device));
+    ctx->cur = 0;
+    ctx->prev = 1;
+    if (int rc = upload(ctx, ctx->st[0], current, ctx->comps)) return rc;
+    if (int rc = upload(ctx, ctx->st[1], previous ? previous : current, ctx->comps)) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->state_set = true;
+    return PETTO_OK;
+}
+
+int petto_dev_get_state(petto_ctx* ctx, double* current, double* previous) {
+    CK(cudaSetDevice(ctx->device));
+    if (current)
+        if (int rc = download(ctx, current, ctx->st[ctx->cur], ctx->comps)) return rc;
+    if (previous)
+        if (int rc = download(ctx, previous, ctx->st[ctx->prev], ctx->comps)) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = require_ready(ctx)) return rc;
+    if (int rc = check_kappa(ctx)) return rc;
+    if (int rc = reset_status(ctx)) return rc;
+    const StepCoef k = coef(3, 0.0, 1.0);
+    if (int rc = state_step(ctx, k, ctx->cur, ctx->prev, ctx->r, 0, 0, true)) return rc;
+    if (ctx->mode == PETTO_MODE_FAST) {
+        k_sum_to<<<1, 256, 0, ctx->stream>>>(ctx->partials, ctx->npartials_used, &ctx->status->sumsq);
+        ctx->launches++;
+        CKL();
+    }
+    if (int rc = read_status(ctx)) return rc;
+    if (r_pde) *r_pde = std::sqrt(ctx->status_h->sumsq) / (double)global_nodes(ctx);
+    if (out) {
+        if (int rc = download(ctx, out, ctx->r, ctx->comps)) return rc;
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return PETTO_OK;
+}
+
+// PTParams::validate (state_solver.hpp:25-33)
+static int validate_params(petto_ctx* ctx, const petto_pt_params* p) {
+    if (!(p->dt_pt > 0.0) && p->n_pt > 0) return fail(ctx, PETTO_INVALID, "pt params: dt_pt must be positive");
+    if (!(p->dt_apt > 0.0) && p->n_apt > 0) return fail(ctx, PETTO_INVALID, "pt params: dt_apt must be positive");
+    if (!(p->theta > 0.0)) return fail(ctx, PETTO_INVALID, "pt params: theta must be positive");
+    if (p->n_apt < 0 || p->n_pt < 0 || p->n_apt + p->n_pt < 1)
+        return fail(ctx, PETTO_INVALID, "pt params: need at least one step per loop");
+    return PETTO_OK;
+}
+
+int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* abort_step) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = validate_params(ctx, p)) return rc;
+    if (int rc = require_ready(ctx)) return rc;
+    if (int rc = check_kappa(ctx)) return rc;
+    if (int rc = reset_status(ctx)) return rc;
+    const long long nsteps = p->n_apt + p->n_pt;
+    long long step = 0;
+    const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
+    const StepCoef kp = coef(2, p->dt_pt, p->theta);
+    for (long s = 0; s < p->n_apt; ++s) {
+        // next := previous buffer, written in place; then swap (state_solver.hpp:421, 440)
+        if (int rc = state_step(ctx, ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
+        std::swap(ctx->cur, ctx->prev);
+    }
+    for (long s = 0; s < p->n_pt; ++s) {
+        if (int rc = state_step(ctx, kp, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
+        std::swap(ctx->cur, ctx->prev);
+    }
+    if (int rc = read_status(ctx)) return rc;
+    if (ctx->status_h->first_bad != PETTO_NO_BAD) {
+        const long long fb = ctx->status_h->first_bad;
+        long long at = std::min(((fb + 99) / 100) * 100, nsteps);
+        // the kernels after `at` were skipped: the buffers still hold the state of
+        // step `at`, but our cur/prev indices advanced past it -- rewind the swaps
+        if ((nsteps - at) % 2) std::swap(ctx->cur, ctx->prev);
+        if (abort_step) *abort_step = at;
+        return fail(ctx, PETTO_ABORT, "numerical abort in 'state' at step " + std::to_string(at) +
+                                          ": non-finite values (time step too large?)");
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_params* p, double target,
+                                   long max_iters, petto_solve_stats* stats) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = require_ready(ctx)) return rc;
+    if (int rc = check_kappa(ctx)) return rc;
+    if (int rc = reset_status(ctx)) return rc;
+    ctx->status_h->target = target;
+    ctx->status_h->max_iters = max_iters;
+    CK(cudaMemcpyAsync(ctx->status, ctx->status_h, sizeof(DeviceStatus), cudaMemcpyHostToDevice, ctx->stream));
+    const int spare = 3 - ctx->cur - ctx->prev;
+    const int b[3] = {ctx->cur, spare, ctx->prev};  // u_k lives in b[k % 3]
+    const StepCoef k = mode == 0 ? coef(2, p->dt_pt, p->theta) : coef(p->form ? 1 : 0, p->dt_apt, p->theta);
+    const long long never = LLONG_MAX;
+    long long launched = 0;  // residual evaluations issued
+    long long chunk = 32;
+    while (true) {
+        for (long long c = 0; c < chunk && launched <= max_iters; ++c, ++launched) {
+            const long long it = launched;
+            if (int rc = state_step(ctx, k, b[it % 3], b[(it + 2) % 3], ctx->st[b[(it + 1) % 3]], it + 1, never,
+                                    true))
+                return rc;
+            k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status,
+                                                      ctx->mode == PETTO_MODE_FAST ? ctx->partials : nullptr,
+                                                      ctx->npartials_used);
+            ctx->launches++;
+            CKL();
+        }
+        if (int rc = read_status(ctx)) return rc;
+        if (ctx->status_h->done || launched > max_iters) break;
+        chunk = std::min<long long>(chunk * 2, 4096);
+    }
+    const DeviceStatus& s = *ctx->status_h;
+    const long long n = s.iterations;
+    ctx->cur = b[n % 3];
+    ctx->prev = b[(n + 2) % 3];
+    stats->iterations = (long)n;
+    stats->r_initial = s.r_initial;
+    stats->r_final = s.r_final;
+    stats->converged = s.converged;
+    if (s.aborted)
+        return fail(ctx, PETTO_ABORT,
+                    "numerical abort in 'state' at step " + std::to_string(n) + ": residual norm diverged");
+    return PETTO_OK;
+}
+
+void petto_dev_unit_cell_stiffness(int dim, const double h[3], double nu, double* ke) {
+    const std::vector<double> K = unit_cell_stiffness(dim, h, nu);
+    std::memcpy(ke, K.data(), sizeof(double) * K.size());
+}
+
+double petto_dev_spectral_bound(int dim, const int64_t n[3], const double length[3], double nu, double e_max) {
+    double h[3] = {1.0, 1.0, 1.0};
+    for (int a = 0; a < dim; ++a) h[a] = length[a] / (double)(n[a] - 1);
+    return spectral_bound(dim, h, nu, e_max);
+}
+
+int64_t petto_dev_launch_count(const petto_ctx* ctx) { return ctx->launches; }
+
+int petto_dev_kernel_timing(petto_ctx* ctx, int enable) {
+    CK(cudaSetDevice(ctx->device));
+    if (enable && ctx->ev_pool.empty()) {
+        ctx->ev_pool.resize(512);
+        for (auto& e : ctx->ev_pool) CK(cudaEventCreate(&e));
+    }
+    ctx->timing = enable != 0;
+    ctx->kernel_ms = 0.0;
+    ctx->kernel_launches = 0;
+    ctx->ev_used = 0;
+    return PETTO_OK;
+}
+
+int petto_dev_kernel_stats(petto_ctx* ctx, double* total_ms, int64_t* launches, double* bytes_per_launch,
+                           char* name, int name_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int e = 0; e + 1 < ctx->ev_used; e += 2) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+        ctx->kernel_ms += ms;
+    }
+    ctx->ev_used = 0;
+    if (total_ms) *total_ms = ctx->kernel_ms;
+    if (launches) *launches = ctx->kernel_launches;
+    if (bytes_per_launch) *bytes_per_launch = ctx->bytes_per_launch;
+    if (name && name_cap > 0) std::snprintf(name, (size_t)name_cap, "%s", ctx->kernel_name.c_str());
+    return PETTO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+"""ctypes binding of include/petto_dev.h and a host-side mirror of the reference's
+state-solver interface (StateOperator / StateHistory / hybrid_solve /
+iterate_to_tolerance, /root/reference/proj/include/petto/state_solver.hpp).
+
+The device library is mandatory: importing this module loads
+lib/libpetto_b200.so and creating a context fails loudly without an sm_100 GPU.
+There is no CPU fallback anywhere on this path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+MAX_PHASES = 8
+OK, ABORT, INVALID, ERROR = 0, 1, 2, 3
+MODE_FAST, MODE_REPLICA = 0, 1
+
+
+class NumericalAbort(RuntimeError):
+    """errors.hpp:10-23: carries the field name and the step index."""
+
+    def __init__(self, message, step=None, field="state"):
+        super().__init__(message)
+        self.step = step
+        self.field = field
+
+
+class GridDesc(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("n", C.c_int64 * 3), ("length", C.c_double * 3), ("physics", C.c_int),
+        ("poisson_ratio", C.c_double), ("mode", C.c_int), ("device", C.c_int),
+        ("k_begin", C.c_int64), ("k_end", C.c_int64),
+    ]
+
+
+class PTParams(C.Structure):
+    _fields_ = [("dt_pt", C.c_double), ("dt_apt", C.c_double), ("theta", C.c_double), ("n_apt", C.c_long),
+                ("n_pt", C.c_long), ("form", C.c_int)]
+
+
+class SolveStats(C.Structure):
+    _fields_ = [("iterations", C.c_long), ("r_initial", C.c_double), ("r_final", C.c_double),
+                ("converged", C.c_int)]
+
+
+class Material(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nphases", C.c_int), ("properties", C.c_double * MAX_PHASES),
+                ("poisson_ratio", C.c_double), ("penalty", C.c_double), ("void_floor", C.c_double)]
+
+
+class Targets(C.Structure):
+    _fields_ = [("fractions", C.c_double * MAX_PHASES), ("has_region", C.c_int),
+                ("region_fractions", C.c_double * MAX_PHASES), ("nregion", C.c_int64),
+                ("region_nodes", C.POINTER(C.c_int64))]
+
+
+class Weights(C.Structure):
+    _fields_ = [("alpha_compliance", C.c_double), ("alpha_volume", C.c_double), ("alpha_unity", C.c_double),
+                ("alpha_region", C.c_double), ("normalize_compliance", C.c_int), ("compliance_sign", C.c_int)]
+
+
+class CHParams(C.Structure):
+    _fields_ = [("mobility", C.c_double), ("gamma", C.c_double), ("dt", C.c_double)]
+
+
+class CHStats(C.Structure):
+    _fields_ = [("mass_before", C.c_double), ("mass_preclamp", C.c_double), ("mass_postclamp", C.c_double)]
+
+
+class Report(C.Structure):
+    _fields_ = [("compliance", C.c_double), ("volume", C.c_double), ("unity", C.c_double), ("region", C.c_double),
+                ("volume_fractions", C.c_double * MAX_PHASES)]
+
+
+class Schedule(C.Structure):
+    _fields_ = [("pt", PTParams), ("ch", CHParams), ("max_loops", C.c_long), ("convergence_tol", C.c_double),
+                ("convergence_window", C.c_int), ("report_every", C.c_int)]
+
+
+class Record(C.Structure):
+    _fields_ = [("loop", C.c_long), ("apt_steps", C.c_longlong), ("pt_steps", C.c_longlong),
+                ("compliance", C.c_double), ("volume", C.c_double), ("unity", C.c_double), ("region", C.c_double),
+                ("r_pde", C.c_double), ("separation", C.c_double), ("volume_fractions", C.c_double * MAX_PHASES),
+                ("wall_seconds", C.c_double)]
+
+
+class RunResult(C.Structure):
+    _fields_ = [("loops", C.c_long), ("apt_steps", C.c_longlong), ("pt_steps", C.c_longlong),
+                ("design_updates", C.c_longlong), ("ch_steps", C.c_longlong), ("clamp_mass_drift", C.c_double),
+                ("termination", C.c_int), ("abort_detail", C.c_char * 256)]
+
+
+RECORD_CB = C.CFUNCTYPE(None, C.POINTER(Record), C.c_void_p)
+
+_lib = None
+
+
+def lib():
+    """Load (building if stale, when nvcc is present) the sm_100a library."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if _build.stale():
+            try:
+                path = _build.build()
+            except Exception:
+                if not os.path.exists(path):
+                    raise
+        L = C.CDLL(path)
+        L.petto_dev_version.restype = C.c_char_p
+        L.petto_dev_last_error.restype = C.c_char_p
+        L.petto_dev_last_error.argtypes = [C.c_void_p]
+        L.petto_dev_stream.restype = C.c_void_p
+        L.petto_dev_stream.argtypes = [C.c_void_p]
+        L.petto_dev_spectral_bound.restype = C.c_double
+        L.petto_dev_spectral_bound.argtypes = [C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_double,
+                                               C.c_double]
+        L.petto_dev_launch_count.restype = C.c_int64
+        L.petto_dev_launch_count.argtypes = [C.c_void_p]
+        for name in ("petto_dev_destroy",):
+            getattr(L, name).argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "petto_dev_version", "petto_dev_device_count", "petto_dev_create", "petto_dev_destroy",
+    "petto_dev_last_error", "petto_dev_stream", "petto_dev_set_mode", "petto_dev_set_constraints",
+    "petto_dev_set_source", "petto_dev_set_property", "petto_dev_init_operator", "petto_dev_set_state",
+    "petto_dev_get_state", "petto_dev_residual", "petto_dev_hybrid_solve", "petto_dev_iterate_to_tolerance",
+    "petto_dev_set_design", "petto_dev_set_phases", "petto_dev_get_phases", "petto_dev_interpolate",
+    "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
+    "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
+    "petto_dev_kernel_timing", "petto_dev_kernel_stats",
+]
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def unit_cell_stiffness(dim, h, nu):
+    n = (1 << dim) * dim
+    out = np.zeros(n * n)
+    lib().petto_dev_unit_cell_stiffness(dim, (C.c_double * 3)(*h), C.c_double(nu), _dp(out))
+    return out.reshape(n, n)
+
+
+def spectral_bound(grid, nu, e_max):
+    """elasticity_spectral_bound (state_solver.hpp:254-279) on the product's host code."""
+    return lib().petto_dev_spectral_bound(grid.dim, (C.c_int64 * 3)(*grid.n), (C.c_double * 3)(*grid.length),
+                                          C.c_double(nu), C.c_double(e_max))
+
+
+def pt_params(p):
+    return PTParams(p.dt_pt, p.dt_apt, p.theta, p.n_apt, p.n_pt, p.form)
+
+
+class Context:
+    """One problem resident in HBM (a petto_ctx)."""
+
+    def __init__(self, grid, physics, poisson_ratio=0.3, mode=MODE_FAST, device=0, k_range=None):
+        L = lib()
+        self.grid = grid
+        self.physics = physics
+        self.comps = grid.dim if physics else 1
+        self.N = grid.num_nodes
+        kb, ke = k_range if k_range else (0, 0)
+        d = GridDesc(grid.dim, (C.c_int64 * 3)(*grid.n), (C.c_double * 3)(*grid.length), physics, poisson_ratio,
+                     mode, device, kb, ke)
+        h = C.c_void_p()
+        rc = L.petto_dev_create(C.byref(d), C.byref(h))
+        if rc != OK:
+            self._raise(rc, L.petto_dev_last_error(None).decode())
+        self.h = h
+        self._cb_keep = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().petto_dev_destroy(h)
+            self.h = None
+
+    close = __del__
+
+    # -- errors: the reference's exception types ---------------------------
+    def _raise(self, rc, msg=None):
+        if msg is None:
+            msg = lib().petto_dev_last_error(self.h).decode()
+        if rc == ABORT:
+            step = None
+            if " at step " in msg:
+                try:
+                    step = int(msg.split(" at step ")[1].split(":")[0])
+                except ValueError:
+                    pass
+            raise NumericalAbort(msg, step)
+        if rc == INVALID:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    def _check(self, rc):
+        if rc != OK:
+            self._raise(rc)
+
+    # -- uploads -------------------------------------------------------------
+    def set_mode(self, mode):
+        self._check(lib().petto_dev_set_mode(self.h, mode))
+
+    def set_constraints(self, entries, values):
+        e = np.ascontiguousarray(entries, dtype=np.int64)
+        v = _f64(values)
+        self._check(lib().petto_dev_set_constraints(self.h, e.ctypes.data_as(C.POINTER(C.c_int64)), _dp(v),
+                                                    C.c_int64(len(e))))
+
+    def set_source(self, source):
+        self._check(lib().petto_dev_set_source(self.h, _dp(_f64(source))))
+
+    def set_property(self, prop):
+        self._check(lib().petto_dev_set_property(self.h, _dp(_f64(prop))))
+
+    def init_operator(self):
+        self._check(lib().petto_dev_init_operator(self.h))
+
+    def set_state(self, cur, prev=None):
+        c = _f64(cur)
+        p = _f64(prev) if prev is not None else c
+        self._check(lib().petto_dev_set_state(self.h, _dp(c), _dp(p)))
+
+    def get_state(self):
+        c = np.zeros(self.comps * self.N)
+        p = np.zeros(self.comps * self.N)
+        self._check(lib().petto_dev_get_state(self.h, _dp(c), _dp(p)))
+        return c, p
+
+    # -- state solve -----------------------------------------------------------
+    def residual(self):
+        out = np.zeros(self.comps * self.N)
+        r = C.c_double(0.0)
+        self._check(lib().petto_dev_residual(self.h, _dp(out), C.byref(r)))
+        return out, r.value
+
+    def hybrid_solve(self, params):
+        step = C.c_int64(0)
+        self._check(lib().petto_dev_hybrid_solve(self.h, C.byref(pt_params(params)), C.byref(step)))
+
+    def iterate_to_tolerance(self, mode, params, target, max_iters):
+        st = SolveStats()
+        self._check(lib().petto_dev_iterate_to_tolerance(self.h, int(mode), C.byref(pt_params(params)),
+                                                         C.c_double(target), C.c_long(max_iters), C.byref(st)))
+        return st
+
+    # -- instrumentation -------------------------------------------------------
+    def stream(self):
+        return lib().petto_dev_stream(self.h)
+
+    def launch_count(self):
+        return lib().petto_dev_launch_count(self.h)
+
+    def kernel_timing(self, enable=True):
+        self._check(lib().petto_dev_kernel_timing(self.h, 1 if enable else 0))
+
+    def kernel_stats(self):
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        name = C.create_string_buffer(64)
+        self._check(lib().petto_dev_kernel_stats(self.h, C.byref(ms), C.byref(n), C.byref(b), name, 64))
+        return ms.value, n.value, b.value, name.value.decode()
+
+
+# ----------------------------------------------------------------------------
+# Host-buffer mirror of the reference's operator interface.
+
+
+@dataclass
+class StateHistory:
+    """StateHistory<double> (state_solver.hpp:37-45) on host arrays."""
+
+    current: np.ndarray
+    previous: np.ndarray
+
+    @staticmethod
+    def of(init):
+        a = _f64(init)
+        return StateHistory(a.copy(), a.copy())
+
+
+class DeviceOperator:
+    """A StateOperator (state_solver.hpp:65-72) whose residual runs on the B200."""
+
+    def __init__(self, grid, physics, prop, source, bc, poisson_ratio=0.3, mode=MODE_FAST):
+        from .problem import make_constraints
+
+        self.grid = grid
+        self.ctx = Context(grid, physics, poisson_ratio, mode)
+        self._comps = self.ctx.comps
+        self.cs = make_constraints(grid, bc, self._comps)
+        self.ctx.set_constraints(*self.cs)
+        self.ctx.set_source(source)
+        self.ctx.set_property(prop)
+        self.ctx.init_operator()
+
+    def components(self):
+        return self._comps
+
+    def constraints(self):
+        return self.cs
+
+    def residual(self, state):
+        self.ctx.set_state(state, state)
+        return self.ctx.residual()[0]
+
+
+def HeatOperator(grid, kappa, source, bc, mode=MODE_FAST):
+    """HeatOperator (state_solver.hpp:76-95)."""
+    return DeviceOperator(grid, 0, kappa, source, bc, mode=mode)
+
+
+def ElasticityOperator(grid, modulus, nu, loads, bc, mode=MODE_FAST):
+    """ElasticityOperator built from a Young's modulus field via make_lame (state_solver.hpp:289-325)."""
+    return DeviceOperator(grid, 1, modulus, loads, bc, poisson_ratio=nu, mode=mode)
+
+
+def residual_norm(r, nodes):
+    """residual_norm (state_solver.hpp:49-58) -- host helper for host arrays."""
+    r = _f64(r)
+    return float(np.sqrt(np.dot(r, r)) / nodes)
+
+
+def hybrid_solve(hist: StateHistory, op: DeviceOperator, params):
+    """hybrid_solve (state_solver.hpp:480-498): uploads the history, runs on the
+    device, downloads the new history (also on NumericalAbort)."""
+    op.ctx.set_state(hist.current, hist.previous)
+    try:
+        op.ctx.hybrid_solve(params)
+    finally:
+        hist.current, hist.previous = op.ctx.get_state()
+
+
+def iterate_to_tolerance(hist: StateHistory, op: DeviceOperator, mode, params, target, max_iters):
+    """iterate_to_tolerance (state_solver.hpp:511-541)."""
+    op.ctx.set_state(hist.current, hist.previous)
+    try:
+        return op.ctx.iterate_to_tolerance(mode, params, target, max_iters)
+    finally:
+        hist.current, hist.previous = op.ctx.get_state()

@@ -1,0 +1,256 @@
+"""GPU parity of the state path through the C-ABI.
+
+REPLICA mode must be bit-identical to the oracle (which is pinned bitwise to the
+reference in test_oracle_port.py).  FAST mode (the fused sm_100a kernels) must
+agree to 1e-12 relative per residual / step and 1e-10 after a few hundred steps
+(SURVEY.md 8c "fast mode" tolerances).
+"""
+import numpy as np
+import pytest
+
+from paper_2509_06971_b200 import device as D
+from paper_2509_06971_b200 import problem as P
+
+from . import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+FAST, REPLICA = D.MODE_FAST, D.MODE_REPLICA
+
+
+def rel_err(a, b):
+    scale = max(np.abs(b).max(), 1e-300)
+    return float(np.abs(a - b).max() / scale)
+
+
+ELASTIC_GRIDS = [
+    P.Grid.make2d(17, 9, 2.0, 1.0),
+    P.Grid.make2d(33, 20, 4.0, 1.0),
+    P.Grid.make3d(7, 6, 5, 1.0, 0.8, 0.6),
+    P.Grid.make3d(12, 9, 10, 2.0, 1.0, 1.0),
+    P.Grid.make3d(37, 15, 11, 2.0, 1.0, 0.7),   # nx > 32, ragged tiles
+    P.Grid.make3d(70, 23, 19, 2.0, 1.0, 1.0),   # several x tiles and strips
+]
+
+
+def elastic_case(g, seed):
+    d = g.dim
+    E = H.random_modulus(g, seed=seed + 1)
+    u = H.random_field(d * g.num_nodes, seed=7 + seed)
+    up = H.random_field(d * g.num_nodes, seed=17 + seed)
+    f = H.sparse_loads(g, d, seed=3 + seed)
+    bc = H.elastic_bc(g, "x_hi", pins=[(g.node(0, 0), 1, 0.0), (g.node(1, 2), 0, 0.25)])
+    return E, u, up, f, bc
+
+
+@pytest.mark.parametrize("gi", range(len(ELASTIC_GRIDS)))
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+def test_elasticity_residual(port, gi, mode):
+    g = ELASTIC_GRIDS[gi]
+    E, u, _, f, bc = elastic_case(g, gi)
+    want = port.elasticity_residual(g, bc, E, 0.3, f, u)
+    op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=mode)
+    got = op.residual(u)
+    if mode == REPLICA:
+        assert np.array_equal(got, want)
+    else:
+        assert rel_err(got, want) < 1e-12
+
+
+HEAT_GRIDS = [P.Grid.make2d(16, 16, 4.0, 4.0), P.Grid.make2d(45, 31, 1.0, 1.0), P.Grid.make3d(9, 8, 7, 1.0, 1.0, 1.0)]
+
+
+@pytest.mark.parametrize("gi", range(len(HEAT_GRIDS)))
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+@pytest.mark.parametrize("uniform", [True, False])
+def test_heat_residual(port, gi, mode, uniform):
+    g = HEAT_GRIDS[gi]
+    kappa = H.rng(gi).uniform(0.5, 2.0, g.num_nodes)
+    src = np.full(g.num_nodes, 0.01) if uniform else H.rng(gi + 9).uniform(-1, 1, g.num_nodes)
+    T = H.random_field(g.num_nodes, 11 + gi, -1, 1)
+    bc = H.heat_bc(g)
+    want = port.heat_residual(g, bc, kappa, src, T)
+    got = D.HeatOperator(g, kappa, src, bc, mode=mode).residual(T)
+    if mode == REPLICA:
+        assert np.array_equal(got, want)
+    else:
+        assert rel_err(got, want) < 1e-12
+
+
+def test_heat_residual_known_answer():
+    """tests/test_state_solver.cpp:51-61: 0.01 at free nodes, 0 at pinned."""
+    g = P.Grid.make2d(16, 16, 4.0, 4.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    for mode in (REPLICA, FAST):
+        r = D.HeatOperator(g, np.ones(g.num_nodes), np.full(g.num_nodes, 0.01), bc, mode=mode).residual(
+            np.zeros(g.num_nodes))
+        pinned = np.zeros(g.num_nodes, bool)
+        pinned[P.make_constraints(g, bc, 1)[0]] = True
+        assert np.all(r[pinned] == 0.0) and np.all(r[~pinned] == 0.01)
+
+
+def test_elasticity_zero_state_known_answer():
+    """tests/test_state_solver.cpp:153-177: r = 0 without loads, -1 on y under f_y = 1."""
+    g = P.Grid.make2d(17, 9, 2.0, 1.0)
+    bc = H.elastic_bc(g, None, pins=[(g.node(0, 0), 1, 0.0)])
+    for mode in (REPLICA, FAST):
+        loads = np.zeros(2 * g.num_nodes)
+        op = D.ElasticityOperator(g, np.ones(g.num_nodes), 0.3, loads, bc, mode=mode)
+        assert np.all(op.residual(np.zeros(2 * g.num_nodes)) == 0.0)
+        loads[g.num_nodes:] = 1.0
+        op = D.ElasticityOperator(g, np.ones(g.num_nodes), 0.3, loads, bc, mode=mode)
+        r = op.residual(np.zeros(2 * g.num_nodes))
+        assert np.all(r[: g.num_nodes] == 0.0)
+        want = np.full(g.num_nodes, -1.0)
+        want[g.node(0, 0)] = 0.0
+        assert np.array_equal(r[g.num_nodes:], want)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_elasticity_annihilates_affine(dim):
+    """tests/test_state_solver.cpp:187-217 on the fast kernels."""
+    g = P.Grid.make2d(9, 7, 1.0, 0.8) if dim == 2 else P.Grid.make3d(7, 6, 5, 1.0, 0.8, 0.6)
+    bc = H.elastic_bc(g, None, pins=[(0, 0, 0.0)])
+    grad = [[0.3, -0.1, 0.05], [0.2, 0.4, -0.15], [0.1, 0.0, 0.25]]
+    i, j, k = g.ijk()
+    x, y, z = (g.spacing[0] * i, g.spacing[1] * j, g.spacing[2] * k)
+    u = np.concatenate([0.7 + grad[c][0] * x + grad[c][1] * y + (grad[c][2] * z if dim == 3 else 0) for c in range(dim)])
+    for mode in (REPLICA, FAST):
+        r = D.ElasticityOperator(g, np.ones(g.num_nodes), 0.3, np.zeros(dim * g.num_nodes), bc, mode=mode).residual(u)
+        r = r.reshape(dim, g.n[2], g.n[1], g.n[0])
+        inner = r[:, 1:-1, 1:-1, 1:-1] if dim == 3 else r[:, :, 1:-1, 1:-1]
+        assert np.abs(inner).max() < 1e-10
+
+
+def test_nonpositive_lame_rejected():
+    g = P.Grid.make2d(5, 5, 1.0, 1.0)
+    E = np.ones(g.num_nodes)
+    E[7] = 0.0
+    with pytest.raises(ValueError, match="Lame fields must be positive"):
+        D.ElasticityOperator(g, E, 0.3, np.zeros(2 * g.num_nodes), H.elastic_bc(g, None))
+
+
+HYBRID_CASES = [
+    (0, 0, P.Grid.make2d(20, 12, 1.0, 1.0)),
+    (0, 1, P.Grid.make3d(9, 7, 6, 1.0, 0.8, 0.6)),
+    (1, 1, P.Grid.make2d(33, 17, 2.0, 1.0)),
+    (1, 0, P.Grid.make2d(20, 12, 1.0, 1.0)),
+    (1, 1, P.Grid.make3d(9, 7, 6, 1.0, 0.8, 0.6)),
+    (1, 1, P.Grid.make3d(40, 17, 12, 2.0, 1.0, 0.7)),
+    (1, 0, P.Grid.make3d(40, 17, 12, 2.0, 1.0, 0.7)),
+]
+
+
+def hybrid_inputs(physics, g):
+    comps = g.dim if physics else 1
+    prop = H.random_modulus(g, 5) if physics else H.rng(4).uniform(0.5, 2.0, g.num_nodes)
+    src = H.sparse_loads(g, comps, 2) if physics else np.full(g.num_nodes, 0.3)
+    bc = H.elastic_bc(g, "x_lo") if physics else H.heat_bc(g)
+    cur = H.random_field(comps * g.num_nodes, 1, -0.01, 0.01)
+    prev = H.random_field(comps * g.num_nodes, 2, -0.01, 0.01)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=37, n_pt=23)
+    return comps, prop, src, bc, cur, prev, p
+
+
+@pytest.mark.parametrize("case", range(len(HYBRID_CASES)))
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+def test_hybrid_solve(port, case, mode):
+    physics, form, g = HYBRID_CASES[case]
+    comps, prop, src, bc, cur, prev, p = hybrid_inputs(physics, g)
+    p.form = form
+    rc, wc, wp, _ = port.hybrid_solve(physics, g, bc, prop, 0.3, src, cur, prev, p)
+    assert rc == 0
+    op = D.DeviceOperator(g, physics, prop, src, bc, mode=mode)
+    hist = D.StateHistory(cur.copy(), prev.copy())
+    D.hybrid_solve(hist, op, p)
+    if mode == REPLICA:
+        assert np.array_equal(hist.current, wc) and np.array_equal(hist.previous, wp)
+    else:
+        assert rel_err(hist.current, wc) < 1e-10 and rel_err(hist.previous, wp) < 1e-10
+
+
+def test_hybrid_zero_apt_equals_plain_pt(port):
+    """tests/test_state_solver.cpp:230-249: n_apt = 0 is 25 PT steps bit for bit."""
+    g = P.Grid.make2d(16, 16, 1.0, 1.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 4, dt_apt=h / 2, theta=1.0, n_apt=0, n_pt=25)
+    op = D.HeatOperator(g, np.ones(g.num_nodes), np.ones(g.num_nodes), bc, mode=REPLICA)
+    hist = D.StateHistory.of(np.zeros(g.num_nodes))
+    D.hybrid_solve(hist, op, p)
+    _, wc, _, _ = port.hybrid_solve(0, g, bc, np.ones(g.num_nodes), 0.3, np.ones(g.num_nodes),
+                                    np.zeros(g.num_nodes), np.zeros(g.num_nodes), p)
+    assert np.array_equal(hist.current, wc)
+
+
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+def test_reckless_step_aborts_at_check(mode):
+    """tests/test_state_solver.cpp:330-340: NumericalAbort at the first check (step 100)."""
+    g = P.Grid.make2d(16, 16, 1.0, 1.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    p = P.PTParams(dt_pt=1e6, dt_apt=0.5 / 15, theta=1.0, n_apt=0, n_pt=5000)
+    op = D.HeatOperator(g, np.ones(g.num_nodes), np.ones(g.num_nodes), bc, mode=mode)
+    hist = D.StateHistory.of(np.zeros(g.num_nodes))
+    with pytest.raises(D.NumericalAbort) as ei:
+        D.hybrid_solve(hist, op, p)
+    assert ei.value.step == 100
+
+
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+def test_constrained_entries_exact_every_step(mode):
+    """tests/test_state_solver.cpp:305-328: pinned entries stay bit-exact."""
+    g = P.Grid.make2d(16, 12, 1.0, 1.0)
+    bc = P.BoundarySpec()
+    bc.face[0] = P.FaceCondition(P.DIRICHLET, 1.25, 0)
+    bc.face[1] = P.FaceCondition(P.NEUMANN_ZERO, 0.0, 0)
+    bc.face[2] = P.FaceCondition(P.DIRICHLET, -0.5, 0)
+    bc.face[3] = P.FaceCondition(P.NEUMANN_ZERO, 0.0, 0)
+    e, v = P.make_constraints(g, bc, 1)
+    op = D.HeatOperator(g, np.ones(g.num_nodes), np.full(g.num_nodes, 0.3), bc, mode=mode)
+    h = g.min_spacing()
+    T = np.zeros(g.num_nodes)
+    T[e] = v
+    hist = D.StateHistory.of(T)
+    for s in range(10):
+        p = P.PTParams(dt_pt=h * h / 4, dt_apt=h / 2, theta=1.0, n_apt=s % 2, n_pt=1 - s % 2)
+        D.hybrid_solve(hist, op, p)
+        assert np.array_equal(hist.current[e], v)
+
+
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+@pytest.mark.parametrize("it_mode", [0, 1])
+def test_iterate_to_tolerance_counts(port, mode, it_mode):
+    g = P.Grid.make2d(24, 24, 1.0, 1.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 4, dt_apt=h / 2, theta=1.0, form=0)
+    z = np.zeros(g.num_nodes)
+    one = np.ones(g.num_nodes)
+    rc, want, wc, wp = port.iterate_to_tolerance(0, g, bc, one, 0.3, one, z, z, it_mode, p, 1e-6, 100000)
+    op = D.HeatOperator(g, one, one, bc, mode=mode)
+    hist = D.StateHistory.of(z)
+    got = D.iterate_to_tolerance(hist, op, it_mode, p, 1e-6, 100000)
+    assert got.converged and want.converged
+    if mode == REPLICA:
+        assert got.iterations == want.iterations and got.r_final == want.r_final
+        assert got.r_initial == want.r_initial
+        assert np.array_equal(hist.current, wc) and np.array_equal(hist.previous, wp)
+    else:
+        assert abs(got.iterations - want.iterations) <= 1
+        assert abs(got.r_initial - want.r_initial) <= 1e-14 * want.r_initial
+
+
+def test_iterate_to_tolerance_elastic_mms_fast(port):
+    """Elasticity with semi-implicit APT converges in the same count (+-1) as the oracle."""
+    g = P.Grid.make3d(12, 9, 10, 2.0, 1.0, 1.0)
+    E, _, _, f, bc = elastic_case(g, 0)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.2 * h, theta=1.0, form=1)
+    z = np.zeros(3 * g.num_nodes)
+    rc, want, _, _ = port.iterate_to_tolerance(1, g, bc, E, 0.3, f, z, z, 1, p, 1e-3, 3000)
+    op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=FAST)
+    hist = D.StateHistory.of(z)
+    got = D.iterate_to_tolerance(hist, op, 1, p, 1e-3, 3000)
+    assert got.converged == want.converged
+    assert abs(got.iterations - want.iterations) <= 1
