@@ -68,7 +68,12 @@ struct petto_ctx {
     double* gc = nullptr;          // P x Ns compliance sensitivity
     double* scratch1 = nullptr;    // Ns
     double* scratch2 = nullptr;    // Ns
-    long long* region_dev = nullptr;
+    long long* region_dev = nullptr;   // region node list (global ids, list order)
+    unsigned char* region_mask = nullptr;  // per stored node: in region
+    double* term1 = nullptr;       // per-owned-node reduction terms
+    double* term2 = nullptr;
+    double* pmax = nullptr;        // per-block maxima [blocks][8]
+    unsigned long long* count = nullptr;
     double* dscal = nullptr;       // device scalars for the design kernels
 
     // instrumentation

@@ -1,9 +1,415 @@
-// design.cuh -- design-subsystem kernels (placeholder until the device loop lands).
+// design.cuh -- design-subsystem kernels: property interpolation, sensitivities
+// + clamped design update, Cahn-Hilliard step, record-time objectives.
+//
+// Reference: include/petto/objectives.hpp:80-480, phase_field.hpp:50-176,
+// optimizer.hpp:95-112.  Per-node terms are computed in parallel with the
+// reference's expression order (radd/rmul: no contraction), and every
+// order-sensitive sum goes through sum_terms(): a single-thread k,j,i-order sum in
+// REPLICA mode (bit-exact with the reference's threads == 1 path) or a fixed-shape
+// tree in FAST mode.  Max-reductions and counts are order-free.
 #pragma once
 
+#include "common.cuh"
 #include "context.hpp"
 
 namespace petto_b200 {
+
+#define PETTO_PI 3.141592653589793238462643383279502884
+
+struct DesignP {
+    int np;
+    double props[8];
+    double penalty;
+    int ipen;          // integer exponent 0..8 of pow_penalty, or -1
+    int ipen1;         // same for penalty - 1
+    double floor_v;
+};
+
+// detail::pow_penalty (objectives.hpp:80-89)
+__device__ __forceinline__ double pow_pen(double x, double e, int ie) {
+    if (ie >= 0) {
+        double r = 1.0;
+        for (int i = 0; i < ie; ++i) r = rmul(r, x);
+        return r;
+    }
+    return pow(x, e);
+}
+
+// compact owned index t -> (i, j, k) and the stored (pitched) index
+__device__ __forceinline__ long long owned_ijk(const Geo& g, long long t, int& i, int& j, int& k) {
+    const long long plane = (long long)g.nx * g.ny;
+    k = g.kb + (int)(t / plane);
+    const long long r = t - (long long)(k - g.kb) * plane;
+    j = (int)(r / g.nx);
+    i = (int)(r - (long long)j * g.nx);
+    return lidx(g, i, j, k);
+}
+
+// interpolate_into (objectives.hpp:95-116) over every stored plane.
+__global__ void k_interpolate(Geo g, DesignP d, const double* __restrict__ ph, double* __restrict__ prop) {
+    const long long plane = (long long)g.nx * g.ny;
+    const long long n = plane * g.nzs;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int k = g.ks0 + (int)(t / plane);
+    const long long r = t - (long long)(k - g.ks0) * plane;
+    const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
+    const long long node = lidx(g, i, j, k);
+    double acc = 0.0;
+    for (int q = 0; q < d.np; ++q) acc = radd(acc, rmul(d.props[q], pow_pen(ph[q * g.Ns + node], d.penalty, d.ipen)));
+    prop[node] = acc > d.floor_v ? acc : d.floor_v;
+}
+
+// detail::d1_along (stencil.hpp:23-31) on the pitched layout.
+__device__ __forceinline__ double d1(const double* f, int t, int n, long long s, double hih) {
+    if (n == 1) return 0.0;
+    if (t == 0) return rmul(rsub(radd(rmul(-3.0, f[0]), rmul(4.0, f[s])), f[2 * s]), hih);
+    if (t == n - 1) return rmul(radd(rsub(rmul(3.0, f[0]), rmul(4.0, f[-s])), f[-2 * s]), hih);
+    return rmul(rsub(f[s], f[-s]), hih);
+}
+
+// Energy-density factor of sensitivities (objectives.hpp:345-375): |grad T|^2 or
+// ctr tr(eps)^2 + cec eps:eps with strain_invariants (:151-180).
+__device__ double energy_factor(const Geo& g, int kind, const double* st, long long node, int i, int j, int k,
+                                double ctr, double cec) {
+    const long long s[3] = {1, g.px, (long long)g.px * g.ny};
+    const int idx[3] = {i, j, k};
+    const int n[3] = {g.nx, g.ny, g.nz};
+    double hih[3];
+    for (int a = 0; a < 3; ++a) hih[a] = rdiv(0.5, g.h[a]);
+    const int d = g.dim;
+    if (kind == 0) {
+        double gsq = 0.0;
+        for (int a = 0; a < d; ++a) {
+            const double v = d1(st + node, idx[a], n[a], s[a], hih[a]);
+            gsq = radd(gsq, rmul(v, v));
+        }
+        return gsq;
+    }
+    double du[9];
+    for (int c = 0; c < d; ++c)
+        for (int a = 0; a < d; ++a) du[c * d + a] = d1(st + c * g.Ns + node, idx[a], n[a], s[a], hih[a]);
+    double t = 0.0, c2 = 0.0;
+    for (int a = 0; a < d; ++a) {
+        const double eaa = du[a * d + a];
+        t = radd(t, eaa);
+        c2 = radd(c2, rmul(eaa, eaa));
+    }
+    for (int a = 0; a < d; ++a)
+        for (int b = a + 1; b < d; ++b) {
+            const double eab = rmul(0.5, radd(du[a * d + b], du[b * d + a]));
+            c2 = radd(c2, rmul(rmul(2.0, eab), eab));
+        }
+    // returns (tr, c2) packed for the objective: caller decides; here the factor
+    return radd(rmul(rmul(ctr, t), t), rmul(cec, c2));
+}
+
+// strain invariants (tr, eps:eps) for mechanical_compliance (objectives.hpp:183-204)
+__device__ void strain_tr_c2(const Geo& g, const double* st, long long node, int i, int j, int k, double& t,
+                             double& c2) {
+    const long long s[3] = {1, g.px, (long long)g.px * g.ny};
+    const int idx[3] = {i, j, k};
+    const int n[3] = {g.nx, g.ny, g.nz};
+    double hih[3];
+    for (int a = 0; a < 3; ++a) hih[a] = rdiv(0.5, g.h[a]);
+    const int d = g.dim;
+    double du[9];
+    for (int c = 0; c < d; ++c)
+        for (int a = 0; a < d; ++a) du[c * d + a] = d1(st + c * g.Ns + node, idx[a], n[a], s[a], hih[a]);
+    t = 0.0;
+    c2 = 0.0;
+    for (int a = 0; a < d; ++a) {
+        const double eaa = du[a * d + a];
+        t = radd(t, eaa);
+        c2 = radd(c2, rmul(eaa, eaa));
+    }
+    for (int a = 0; a < d; ++a)
+        for (int b = a + 1; b < d; ++b) {
+            const double eab = rmul(0.5, radd(du[a * d + b], du[b * d + a]));
+            c2 = radd(c2, rmul(rmul(2.0, eab), eab));
+        }
+}
+
+// term[t] = phi * cell_volume (phase_mass, phase_field.hpp:84-101), compact order.
+__global__ void k_term_mass(Geo g, const double* __restrict__ phi, double* __restrict__ term) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    term[t] = rmul(phi[node], cell_volume(g, i, j, k));
+}
+
+// single-thread ordered sum (par::serial() branch) / fixed-shape tree partials
+__global__ void k_sum_serial(const double* __restrict__ term, long long n, double* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    double s = 0.0;
+    for (long long t = 0; t < n; ++t) s = radd(s, term[t]);
+    *out = s;
+}
+
+__global__ void k_sum_partials(const double* __restrict__ term, long long n, double* partials) {
+    __shared__ double scratch[32];
+    double s = 0.0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+        s += term[t];
+    const double b = block_sum<8>(s, scratch);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void k_sum_finish(const double* __restrict__ partials, int n, double* out) {
+    __shared__ double scratch[32];
+    double s = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) s += partials[t];
+    const double b = block_sum<8>(s, scratch);
+    if (threadIdx.x == 0) *out = b;
+}
+
+// ------------------------------------------------------------- sensitivities
+
+// gc_i = dprop_i * factor * vol (objectives.hpp:393-420) for every phase, plus
+// block partial maxima of |gc_i| (par::max_abs_nodes, order-free).
+__global__ void k_sens_gc(Geo g, DesignP d, int kind, double ctr, double cec, const double* __restrict__ ph,
+                          const double* __restrict__ st, double* __restrict__ gc, double* __restrict__ pmax) {
+    __shared__ double smax[8][8];
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    double lmax[8];
+    for (int q = 0; q < 8; ++q) lmax[q] = 0.0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
+         t += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        const long long node = owned_ijk(g, t, i, j, k);
+        const double fac = energy_factor(g, kind, st, node, i, j, k, ctr, cec);
+        const double vol = cell_volume(g, i, j, k);
+        double mix = 0.0;
+        for (int q = 0; q < d.np; ++q) mix = radd(mix, rmul(d.props[q], pow_pen(ph[q * g.Ns + node], d.penalty, d.ipen)));
+        for (int q = 0; q < d.np; ++q) {
+            const double dprop =
+                mix > d.floor_v ? rmul(rmul(d.penalty, d.props[q]), pow_pen(ph[q * g.Ns + node], d.penalty - 1.0, d.ipen1))
+                                : 0.0;
+            const double v = rmul(rmul(dprop, fac), vol);
+            gc[q * g.Ns + node] = v;
+            lmax[q] = fmax(lmax[q], fabs(v));
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int q = 0; q < d.np; ++q) {
+        const double m = warp_max(lmax[q]);
+        if (l == 0) smax[q][w] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x < d.np) {
+        double m = 0.0;
+        for (int ww = 0; ww < 8; ++ww) m = fmax(m, smax[threadIdx.x][ww]);
+        pmax[blockIdx.x * 8 + threadIdx.x] = m;
+    }
+}
+
+// Scalars of the update (objectives.hpp:386-398, 424-436, 456-468), computed on
+// the device from the reduced masses / maxima.  dsc layout: see DS_* below.
+enum {
+    DS_MASS = 0,     // [8] phase masses (pre-update)
+    DS_GMAX = 8,     // [8]
+    DS_RACC = 16,    // [8] region sums of phi*vol
+    DS_RVOL = 24,    // region volume
+    DS_CSCALE = 32,  // [8]
+    DS_DM = 40,      // [8]
+    DS_RCOEFF = 48,  // [8]
+    DS_TMP = 56,     // [8] scratch sums
+    DS_DRIFT = 64,   // accumulated clamp mass drift
+    DS_CH = 72,      // [8][3] ch masses: before, pre, post
+    DS_OBJ = 104,    // [4] compliance, unity, separation count, spare
+    DS_COUNT = 128
+};
+
+struct UpdateScal {
+    double inv_vol;
+    double fractions[8];
+    double region_fractions[8];
+    int has_region;
+    double alpha_c, alpha_v, alpha_u, alpha_r;
+    int normalize, sign;
+};
+
+__global__ void k_design_scalars(int np, UpdateScal u, double* dsc, const double* __restrict__ pmax, int nblocks) {
+    if (threadIdx.x || blockIdx.x) return;
+    for (int q = 0; q < np; ++q) {
+        double m = 0.0;
+        for (int b = 0; b < nblocks; ++b) m = fmax(m, pmax[b * 8 + q]);
+        dsc[DS_GMAX + q] = m;
+        const double mean = dsc[DS_MASS + q] * u.inv_vol;  // volume_fractions
+        dsc[DS_DM + q] = (2.0 * (mean - u.fractions[q])) * u.inv_vol;
+        double cs = 0.0;
+        if (u.alpha_c > 0) {
+            if (u.normalize)
+                cs = m > 0 ? (double)u.sign * u.alpha_c / m : 0.0;
+            else
+                cs = (double)u.sign * u.alpha_c;
+        }
+        dsc[DS_CSCALE + q] = cs;
+        if (u.has_region) {
+            const double vb = dsc[DS_RVOL];
+            const double mb = dsc[DS_RACC + q] / vb;
+            dsc[DS_RCOEFF + q] = (2.0 * (mb - u.region_fractions[q])) / vb;
+        }
+    }
+}
+
+// design_update_inplace (objectives.hpp:444-480) with gv/gu/gr formed on the fly
+// from the pre-update phases of the node.
+__global__ void k_design_update(Geo g, int np, UpdateScal u, const double* __restrict__ dsc,
+                                const double* __restrict__ gc, const unsigned char* __restrict__ region,
+                                double* ph) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    const double vol = cell_volume(g, i, j, k);
+    double p[8];
+    double ssum = -1.0;
+    for (int q = 0; q < np; ++q) {
+        p[q] = ph[q * g.Ns + node];
+        ssum = radd(ssum, p[q]);
+    }
+    const double gu = rmul(rmul(2.0, ssum), vol);
+    const bool in_region = u.has_region && region[node];
+    for (int q = 0; q < np; ++q) {
+        const double gv = rmul(dsc[DS_DM + q], vol);
+        double step = radd(radd(rmul(dsc[DS_CSCALE + q], gc[q * g.Ns + node]), rmul(u.alpha_v, gv)), rmul(u.alpha_u, gu));
+        if (u.has_region) {
+            const double gr = in_region ? rmul(dsc[DS_RCOEFF + q], vol) : 0.0;
+            step = radd(step, rmul(u.alpha_r, gr));
+        }
+        const double v = rsub(p[q], step);
+        ph[q * g.Ns + node] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    }
+}
+
+// region sums (region_fractions_measured / region_volume, objectives.hpp:251-288):
+// terms in the region list order.
+__global__ void k_region_terms(Geo g, const long long* __restrict__ nodes, long long n, const double* __restrict__ phi,
+                               double* __restrict__ term) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const long long gn = nodes[t];
+    const long long plane = (long long)g.nx * g.ny;
+    const int k = (int)(gn / plane);
+    const long long r = gn - (long long)k * plane;
+    const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
+    const double cv = cell_volume(g, i, j, k);
+    term[t] = phi ? rmul(phi[lidx(g, i, j, k)], cv) : cv;
+}
+
+// --------------------------------------------------------------- Cahn-Hilliard
+
+// dwell (phase_field.hpp:56-60)
+__device__ __forceinline__ double dwell(double p) {
+    return rmul(PETTO_PI / 64.0, sin(rmul(2.0 * PETTO_PI, p)));
+}
+
+// detail::lap_along (stencil.hpp:109-116)
+__device__ __forceinline__ double lap_along(const double* f, int t, int n, long long s, double inv_h2) {
+    if (n == 1) return 0.0;
+    if (t == 0) return rmul(rmul(2.0, rsub(f[s], f[0])), inv_h2);
+    if (n - 1 == t) return rmul(rmul(2.0, rsub(f[-s], f[0])), inv_h2);
+    return rmul(radd(rsub(f[s], f[0]), rsub(f[-s], f[0])), inv_h2);
+}
+
+__device__ __forceinline__ double lap_noflux(const Geo& g, const double* f, long long node, int i, int j, int k) {
+    double acc = lap_along(f + node, i, g.nx, 1, rdiv(1.0, rmul(g.h[0], g.h[0])));
+    acc = radd(acc, lap_along(f + node, j, g.ny, g.px, rdiv(1.0, rmul(g.h[1], g.h[1]))));
+    if (g.nz > 1) acc = radd(acc, lap_along(f + node, k, g.nz, (long long)g.px * g.ny, rdiv(1.0, rmul(g.h[2], g.h[2]))));
+    return acc;
+}
+
+// chemical_potential_into (phase_field.hpp:63-72): mu = dwell(phi) - gamma lap(phi)
+__global__ void k_chem_potential(Geo g, const double* __restrict__ phi, double gamma, double* __restrict__ mu) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    mu[node] = rsub(dwell(phi[node]), rmul(gamma, lap_noflux(g, phi, node, i, j, k)));
+}
+
+// phi += dt D lap(mu) (phase_field.hpp:147-149); pre-clamp mass terms
+__global__ void k_ch_update(Geo g, const double* __restrict__ mu, double step, double* phi, double* __restrict__ term) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    const double v = radd(phi[node], rmul(step, lap_noflux(g, mu, node, i, j, k)));
+    phi[node] = v;
+    term[t] = rmul(v, cell_volume(g, i, j, k));
+}
+
+// clamp to [0, 1] (phase_field.hpp:151-153); post-clamp mass terms, non-finite flag
+__global__ void k_ch_clamp(Geo g, double* phi, double* __restrict__ term, unsigned* flag) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    const double p = phi[node];
+    const double v = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
+    phi[node] = v;
+    if (!isfinite(v)) atomicOr(flag, 4u);
+    term[t] = rmul(v, cell_volume(g, i, j, k));
+}
+
+// ------------------------------------------------------------------ objectives
+
+// Per-node terms of evaluate_objectives (objectives.hpp:126-247, 304-320):
+// compliance (thermal: kappa |grad T|^2 dV, elastic: (lam tr^2 + 2 mu eps:eps) dV with
+// make_lame of the re-interpolated property), unity (sum phi - 1)^2 dV, and the
+// phase-separation indicator (optimizer.hpp:95-112).
+__global__ void k_objective_terms(Geo g, DesignP d, int kind, double cl, double cm, const double* __restrict__ ph,
+                                  const double* __restrict__ st, double* __restrict__ tcomp,
+                                  double* __restrict__ tunity, unsigned long long* sep_count) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool near = false;
+    if (t < owned) {
+        int i, j, k;
+        const long long node = owned_ijk(g, t, i, j, k);
+        const double cv = cell_volume(g, i, j, k);
+        double acc = 0.0, s = -1.0, worst = 0.0;
+        for (int q = 0; q < d.np; ++q) {
+            const double p = ph[q * g.Ns + node];
+            acc = radd(acc, rmul(d.props[q], pow_pen(p, d.penalty, d.ipen)));
+            s = radd(s, p);
+            const double dd = p < rsub(1.0, p) ? p : rsub(1.0, p);
+            if (dd > worst) worst = dd;
+        }
+        near = worst < 0.1;
+        const double E = acc > d.floor_v ? acc : d.floor_v;
+        double c;
+        if (kind == 0) {
+            c = rmul(rmul(E, energy_factor(g, 0, st, node, i, j, k, 0.0, 0.0)), cv);
+        } else {
+            double tr, c2;
+            strain_tr_c2(g, st, node, i, j, k, tr, c2);
+            const double lam = rmul(cl, E), mu = rmul(cm, E);
+            c = rmul(radd(rmul(rmul(lam, tr), tr), rmul(rmul(2.0, mu), c2)), cv);
+        }
+        tcomp[t] = c;
+        tunity[t] = rmul(rmul(s, s), cv);
+    }
+    const unsigned cnt = __popc(__ballot_sync(0xffffffffu, near));
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(sep_count, (unsigned long long)cnt);
+}
+
+__global__ void k_check_finite_phases(Geo g, int np, const double* __restrict__ ph, unsigned* flag) {
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= owned) return;
+    int i, j, k;
+    const long long node = owned_ijk(g, t, i, j, k);
+    for (int q = 0; q < np; ++q)
+        if (!isfinite(ph[q * g.Ns + node])) atomicOr(flag, 4u);
+}
 
 inline void design_free(petto_ctx* ctx) {
     cudaFree(ctx->phases);
@@ -11,8 +417,14 @@ inline void design_free(petto_ctx* ctx) {
     cudaFree(ctx->scratch1);
     cudaFree(ctx->scratch2);
     cudaFree(ctx->region_dev);
+    cudaFree(ctx->region_mask);
+    cudaFree(ctx->term1);
+    cudaFree(ctx->term2);
+    cudaFree(ctx->pmax);
     ctx->phases = ctx->gc = ctx->scratch1 = ctx->scratch2 = nullptr;
+    ctx->term1 = ctx->term2 = ctx->pmax = nullptr;
     ctx->region_dev = nullptr;
+    ctx->region_mask = nullptr;
 }
 
 }  // namespace petto_b200

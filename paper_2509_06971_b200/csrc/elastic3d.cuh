@@ -10,19 +10,22 @@
 //   * the unit-cell stiffness is applied in the Walsh-Hadamard corner-parity
 //     basis, where it has 45 structural nonzeros (stiffness.hpp); the forward and
 //     inverse transforms factor into x/y/z butterflies;
-//   * CTA = 9 warps: lane l <-> x = i0 + l (32 nodes), warp w <-> row j0-1+w
+//   * CTA = 8 warps: lane l <-> x = i0 + l (32 nodes), warp w <-> row j0-1+w
 //     (warp 0 is the y-halo row of cells whose top corners feed row j0);
 //   * each CTA streams along z (the outermost axis): per cell plane it keeps the
 //     previous plane's y/x-butterflies (12+1 doubles) and the top-face
-//     contributions (12 doubles) in registers;
+//     contributions (12 doubles) in registers, alternating two register sets so
+//     the stream needs no copies;
 //   * node planes arrive by TMA (cp.async.bulk.tensor, zero-filled outside the
 //     grid) into a 5-stage shared-memory ring guarded by mbarriers, issued 4
 //     tasks ahead by one elected thread;
 //   * x-neighbour contributions travel by warp shuffle, y-neighbour ones through
-//     a double-buffered shared tile, and the contribution of the previous x-tile's
-//     last column through a small shared "x-halo" array -- CTAs walk the x-tiles
-//     of their (strip, z-run) sequentially, so no cell is computed twice in x;
-//   * work = (y-strip, plane) units split evenly over a persistent grid.
+//     a double-buffered shared tile, and the previous x-tile's last column through
+//     a small shared "x-halo" array -- a CTA walks the x-tiles of its
+//     (strip, z-chunk) item sequentially, so no cell is computed twice in x;
+//   * work item = (y-strip, z-chunk); item b -> CTA b with strips fastest, so the
+//     CTAs sharing a strip boundary stream the same planes at the same time and
+//     the halo rows are served from L2.
 // Algorithmic HBM bytes per node-update: u_n 24 + u_{n-1} 24 + E 8 + u_{n+1} 24
 // (+1 mask byte); PT drops u_{n-1}.
 #pragma once
@@ -38,7 +41,7 @@ constexpr int NTHREADS = NWARP * 32;
 constexpr int BOXX = 34;       // TMA box width (33 columns used; 16-byte multiple)
 constexpr int UROWS = W + 2;   // rows j0-1 .. j0+W
 constexpr int S = 5;           // pipeline depth
-constexpr int LMAX = 64;       // longest z sub-run (x-halo buffer)
+constexpr int LMAX = 64;       // longest z chunk (x-halo buffer)
 
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
 constexpr int OFF_U = 0;                                    // [3][UROWS][BOXX] f64
@@ -54,289 +57,379 @@ constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][6][32]
 constexpr int OFF_X = OFF_Y + 2 * NWARP * 6 * 32 * 8;       // [2][LMAX][NWARP][3] f64
 constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] mbarriers
 constexpr int OFF_RED = OFF_BAR + S * 8;                    // [NWARP] f64
-constexpr int OFF_PIT = OFF_RED + 16 * 8;                   // producer cursor
-constexpr int SMEM_BYTES = OFF_PIT + 64;
+constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
+constexpr int SMEM_BYTES = OFF_CUR + 64;
 
 struct Params {
     Geo g;
     double kh[45];     // modal stiffness (stiffness.hpp pattern order)
     double e_scale;    // (sum of 8 corner E) -> E_cell: cm * 2(1+nu_op) / 8
     double inv_base;   // 1 / (hx hy hz)
-    int form;          // 0 APT explicit, 1 APT semi-implicit, 2 PT, 3 residual only
     double dt, a, b, inv;
     double* next;      // output field (may alias the previous iterate)
     const double* aux; // pinned values / loads (3 x Ns)
     double* partials;  // per-CTA sum of r^2 over unconstrained entries (nullable)
     DeviceStatus* status;
     long long step, nsteps;  // 1-based step index within the solve, total steps
-    int ntx;           // x tiles
-    int nzo;           // owned planes
-    long long units;   // strips * nzo
+    int ntx;           // x tiles of 32 nodes
+    int nstrips;       // y strips of W rows
+    int chunk;         // owned planes per z chunk (<= LMAX)
+    int nitems;        // nstrips * chunks
 };
 
-struct TaskIt {
-    long long u, u_end;
-    int s, ka, len, t, kk;
+// Producer cursor over the CTA's task sequence: items (b, b+grid, ...), x tiles,
+// tasks kc = ka-2 (prologue), ka-1 (first cell plane), ka .. kb-1 (owned planes).
+struct Cursor {
+    int item, t, kk, s, ka, len;
     bool valid;
-
-    __device__ void subrun(const Params& P) {
-        if (u >= u_end) {
-            valid = false;
-            return;
-        }
-        s = (int)(u / P.nzo);
-        ka = P.g.kb + (int)(u - (long long)s * P.nzo);
-        long long lim = (long long)(s + 1) * P.nzo;
-        if (lim > u_end) lim = u_end;
-        long long l = lim - u;
-        len = (int)(l < LMAX ? l : LMAX);
-        t = 0;
-        kk = 0;
-        valid = true;
-    }
-    __device__ void init(const Params& P) {
-        u = (long long)blockIdx.x * P.units / gridDim.x;
-        u_end = (long long)(blockIdx.x + 1) * P.units / gridDim.x;
-        subrun(P);
+    __device__ void set(const Params& P) {
+        valid = item < P.nitems;
+        if (!valid) return;
+        s = item % P.nstrips;
+        ka = P.g.kb + (item / P.nstrips) * P.chunk;
+        len = min(P.chunk, P.g.ke - ka);
     }
     __device__ void next(const Params& P) {
         if (++kk == len + 2) {
             kk = 0;
             if (++t == P.ntx) {
-                u += len;
-                subrun(P);
+                t = 0;
+                item += gridDim.x;
+                set(P);
             }
         }
     }
-    __device__ int kc() const { return ka - 2 + kk; }
 };
 
-__device__ __forceinline__ void issue(const Params& P, const TaskIt& it, unsigned char* smem, uint64_t* bars,
+template <int FORM>
+__device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned char* smem, uint64_t* bars,
                                       int stage, const CUtensorMap* tU, const CUtensorMap* tE,
                                       const CUtensorMap* tP, const CUtensorMap* tM) {
     unsigned char* st = smem + stage * STAGE_BYTES;
-    const bool own = it.kk >= 2;
-    const bool need_p = own && P.form <= 1;
-    uint32_t bytes = BYTES_UE + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
+    const bool own = c.kk >= 2;
+    const bool need_p = own && FORM <= 1;
+    const uint32_t bytes = BYTES_UE + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
     mbar_expect_tx(&bars[stage], bytes);
-    const int i0 = it.t * 32, j0 = it.s * W;
-    const int zn = it.kc() + 1 - P.g.ks0;
+    const int i0 = c.t * 32, j0 = c.s * W, kc = c.ka - 2 + c.kk;
+    const int zn = kc + 1 - P.g.ks0;
     tma_load_4d(st + OFF_U, tU, &bars[stage], i0, j0 - 1, zn, 0);
     tma_load_3d(st + OFF_E, tE, &bars[stage], i0, j0 - 1, zn);
     if (own) {
-        const int zc = it.kc() - P.g.ks0;
-        tma_load_3d(st + OFF_M, tM, &bars[stage], i0, j0, zc);
-        if (need_p) tma_load_4d(st + OFF_P, tP, &bars[stage], i0, j0, zc, 0);
+        tma_load_3d(st + OFF_M, tM, &bars[stage], i0, j0, kc - P.g.ks0);
+        if (need_p) tma_load_4d(st + OFF_P, tP, &bars[stage], i0, j0, kc - P.g.ks0, 0);
     }
 }
 
+// Everything a task needs that is fixed for one x-tile of one item.
+struct Tile {
+    int i, j, t;
+    bool upd;            // this thread owns a grid node of the tile
+    double escale;       // e_scale, or 0 where the cell (i, j) is outside the grid
+    double invv_xy;      // 1/V without the z-end factor
+    long long node0;     // lidx(i, j, 0)
+    double* xw;          // x-halo out (lane 31) / in (lane 0)
+    const double* xr;
+};
+
+struct Pipe {
+    unsigned char* smem;
+    uint64_t* bars;
+    int st, q;
+    uint32_t phase;
+};
+
+// forward x/y butterflies of node plane kc+1 for cell (i, j): B[sx + 2 sy][c], E sum
+__device__ __forceinline__ void forward(const unsigned char* sb, int w, int l, double (&B)[4][3], double& E) {
+    const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double* r0 = su + c * UROWS * BOXX;
+        const double a = r0[0], b = r0[1], cc = r0[BOXX], d = r0[BOXX + 1];
+        const double A0 = a + b, A1 = a - b, A0n = cc + d, A1n = cc - d;
+        B[0][c] = A0 + A0n;
+        B[1][c] = A1 + A1n;
+        B[2][c] = A0 - A0n;
+        B[3][c] = A1 - A1n;
+    }
+    const double* e0 = reinterpret_cast<const double*>(sb + OFF_E) + w * BOXX + l;
+    E = (e0[0] + e0[1]) + (e0[BOXX] + e0[BOXX + 1]);
+}
+
+// z butterflies, modal stiffness, inverse z butterflies: bottom face (node plane
+// kc) returned in face (added to the carried top), new top carried out.
+__device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], double Ec, const double (&Bn)[4][3],
+                                     double En, double escale, double (&top)[4][3], double (&face)[4][3]) {
+    const double ec = (Ec + En) * escale;
+    // modal coefficients C[s] = E_cell * (z butterfly), s = sx + 2 sy + 4 sz; the
+    // modal stiffness decouples into blocks {1,2,4}, {3,5,6}, {7}, evaluated and
+    // consumed one after the other to keep few values live.
+    auto Cp = [&](int q, int c) { return (Bc[q][c] + Bn[q][c]) * ec; };  // sz = 0
+    auto Cm = [&](int q, int c) { return (Bc[q][c] - Bn[q][c]) * ec; };  // sz = 1
+    // block A: linear modes 1 (x), 2 (y), 4 (z)
+    const double c10 = Cp(1, 0), c11 = Cp(1, 1), c12 = Cp(1, 2);
+    const double c20 = Cp(2, 0), c21 = Cp(2, 1), c22 = Cp(2, 2);
+    const double c40 = Cm(0, 0), c41 = Cm(0, 1), c42 = Cm(0, 2);
+    const double F10 = P.kh[0] * c10 + P.kh[1] * c21 + P.kh[2] * c42;
+    const double F11 = P.kh[3] * c11 + P.kh[4] * c20;
+    const double F12 = P.kh[5] * c12 + P.kh[6] * c40;
+    const double F20 = P.kh[7] * c11 + P.kh[8] * c20;
+    const double F21 = P.kh[9] * c10 + P.kh[10] * c21 + P.kh[11] * c42;
+    const double F22 = P.kh[12] * c22 + P.kh[13] * c41;
+    const double F40 = P.kh[14] * c12 + P.kh[15] * c40;
+    const double F41 = P.kh[16] * c22 + P.kh[17] * c41;
+    const double F42 = P.kh[18] * c10 + P.kh[19] * c21 + P.kh[20] * c42;
+    // pair (0, 4): mode 0 (rigid translation) carries no force
+    face[0][0] = top[0][0] + F40;
+    face[0][1] = top[0][1] + F41;
+    face[0][2] = top[0][2] + F42;
+    top[0][0] = -F40;
+    top[0][1] = -F41;
+    top[0][2] = -F42;
+    // block B: bilinear modes 3 (xy), 5 (xz), 6 (yz)
+    const double c30 = Cp(3, 0), c31 = Cp(3, 1), c32 = Cp(3, 2);
+    const double c50 = Cm(1, 0), c51 = Cm(1, 1), c52 = Cm(1, 2);
+    const double c60 = Cm(2, 0), c61 = Cm(2, 1), c62 = Cm(2, 2);
+    const double F30 = P.kh[21] * c30 + P.kh[22] * c62;
+    const double F31 = P.kh[23] * c31 + P.kh[24] * c52;
+    const double F32 = P.kh[25] * c32 + P.kh[26] * c51 + P.kh[27] * c60;
+    const double F50 = P.kh[28] * c50 + P.kh[29] * c61;
+    const double F51 = P.kh[30] * c32 + P.kh[31] * c51 + P.kh[32] * c60;
+    const double F52 = P.kh[33] * c31 + P.kh[34] * c52;
+    const double F60 = P.kh[35] * c32 + P.kh[36] * c51 + P.kh[37] * c60;
+    const double F61 = P.kh[38] * c50 + P.kh[39] * c61;
+    const double F62 = P.kh[40] * c30 + P.kh[41] * c62;
+    // pairs (1, 5) and (2, 6)
+    face[1][0] = top[1][0] + (F10 + F50);
+    face[1][1] = top[1][1] + (F11 + F51);
+    face[1][2] = top[1][2] + (F12 + F52);
+    top[1][0] = F10 - F50;
+    top[1][1] = F11 - F51;
+    top[1][2] = F12 - F52;
+    face[2][0] = top[2][0] + (F20 + F60);
+    face[2][1] = top[2][1] + (F21 + F61);
+    face[2][2] = top[2][2] + (F22 + F62);
+    top[2][0] = F20 - F60;
+    top[2][1] = F21 - F61;
+    top[2][2] = F22 - F62;
+    // block C: trilinear mode 7, pair (3, 7)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double F7 = P.kh[42 + c] * Cm(3, c);
+        const double F3 = c == 0 ? F30 : (c == 1 ? F31 : F32);
+        face[3][c] = top[3][c] + (F3 + F7);
+        top[3][c] = F3 - F7;
+    }
+}
+
+template <int FORM>
+__device__ __forceinline__ void end_task(const Params& P, Pipe& pp, Cursor* pc, const CUtensorMap* tU,
+                                         const CUtensorMap* tE, const CUtensorMap* tP, const CUtensorMap* tM) {
+    __syncthreads();
+    if (threadIdx.x == 0 && pc->valid) {
+        issue<FORM>(P, *pc, pp.smem, pp.bars, pp.st == 0 ? S - 1 : pp.st - 1, tU, tE, tP, tM);
+        pc->next(P);
+    }
+}
+
+__device__ __forceinline__ void advance(Pipe& pp) {
+    ++pp.q;
+    if (++pp.st == S) {
+        pp.st = 0;
+        pp.phase ^= 1u;
+    }
+}
+
+// One owned node plane kc: forward of plane kc+1 into Bn, cell plane kc, face
+// assembly, node update of (i, j, kc).
+template <int FORM>
+__device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, const Tile& T, int kc, int zi,
+                                         const double (&Bc)[4][3], double Ec, double (&Bn)[4][3], double& En,
+                                         double (&top)[4][3], double (&ucar)[3], double& rsq, unsigned& bad,
+                                         double* sY, const CUtensorMap* tU, const CUtensorMap* tE,
+                                         const CUtensorMap* tP, const CUtensorMap* tM) {
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const Geo& g = P.g;
+    mbar_wait(&pp.bars[pp.st], pp.phase);
+    const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
+    forward(sb, w, l, Bn, En);
+    double face[4][3];
+    cell(P, Bc, Ec, Bn, En, kc <= g.nz - 2 ? T.escale : 0.0, top, face);
+    // inverse y butterflies; row j+1's share to warp w+1
+    double* sYw = sY + (pp.q & 1) * (NWARP * 6 * 32);
+    double Yj[2][3];
+#pragma unroll
+    for (int sx = 0; sx < 2; ++sx)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            Yj[sx][c] = face[sx][c] + face[sx + 2][c];
+            sYw[(w * 6 + sx * 3 + c) * 32 + l] = face[sx][c] - face[sx + 2][c];
+        }
+    end_task<FORM>(P, pp, pc, tU, tE, tP, tM);
+    // edge sums (w >= 1), inverse x butterflies, node assembly
+    const double* below = sYw + ((w > 0 ? w - 1 : 0) * 6) * 32 + l;
+    const double wsel = w > 0 ? 1.0 : 0.0;
+    double Xi[3], Xn[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double e0v = Yj[0][c] + wsel * below[c * 32];
+        const double e1v = Yj[1][c] + wsel * below[(3 + c) * 32];
+        Xi[c] = e0v + e1v;
+        Xn[c] = e0v - e1v;
+    }
+    double acc[3];
+    const double* xr = T.xr + zi * (NWARP * 3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double nb = __shfl_up_sync(0xffffffffu, Xn[c], 1);
+        acc[c] = Xi[c] + (l > 0 ? nb : (T.t > 0 ? xr[c] : 0.0));
+    }
+    if (l == 31) {
+        double* xw = T.xw + zi * (NWARP * 3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xw[c] = Xn[c];
+    }
+    if (T.upd) {
+        const unsigned char mk = (sb + OFF_M)[(w - 1) * 32 + l];
+        const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (w - 1) * 32 + l;
+        const double invv = (kc == 0 || kc == g.nz - 1) ? 2.0 * T.invv_xy : T.invv_xy;
+        const long long node = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
+        auto update = [&](int c, double r) {
+            if (FORM == 0) {
+                const double cu = ucar[c], pv = sp[c * W * 32];
+                return 2.0 * cu - pv + P.a * r - P.b * (cu - pv);
+            } else if (FORM == 1) {
+                const double cu = ucar[c], pv = sp[c * W * 32];
+                return (2.0 * cu - pv + P.b * cu + P.a * r) * P.inv;
+            } else if (FORM == 2) {
+                return ucar[c] + P.dt * r;
+            }
+            return r;
+        };
+        double nv[3];
+        if (!mk) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double r = -acc[c] * invv;
+                nv[c] = update(c, r);
+                rsq += r * r;
+            }
+        } else {  // rare: pinned components and/or a load on this node
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const bool pinned = (mk >> c) & 1;
+                const double f = ((mk & 8) && !pinned) ? P.aux[c * g.Ns + node] : 0.0;
+                const double r = -acc[c] * invv - f;
+                if (pinned) {
+                    nv[c] = FORM == 3 ? 0.0 : P.aux[c * g.Ns + node];
+                } else {
+                    rsq += r * r;
+                    nv[c] = update(c, r);
+                }
+            }
+        }
+        // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
+        unsigned ex = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
+            P.next[c * g.Ns + node] = nv[c];
+        }
+        bad |= ex;
+    }
+    // own node of plane kc+1 feeds the next task's update (this stage is only
+    // recycled after the next task's barrier)
+    const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
+    advance(pp);
+}
+
+template <int FORM>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tU,
                      const __grid_constant__ CUtensorMap tE, const __grid_constant__ CUtensorMap tP,
                      const __grid_constant__ CUtensorMap tM) {
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    double* sY = reinterpret_cast<double*>(smem + OFF_Y);
-    double* sX = reinterpret_cast<double*>(smem + OFF_X);
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
     if (skip_step(P.status, P.step, P.nsteps)) return;
-
-    TaskIt it;
-    it.init(P);
+    Pipe pp{smem, reinterpret_cast<uint64_t*>(smem + OFF_BAR), 0, 0, 0u};
+    double* sY = reinterpret_cast<double*>(smem + OFF_Y);
+    double* sX = reinterpret_cast<double*>(smem + OFF_X);
+    Cursor* pc = reinterpret_cast<Cursor*>(smem + OFF_CUR);
     if (threadIdx.x == 0) {
         prefetch_tmap(&tU);
         prefetch_tmap(&tE);
         prefetch_tmap(&tP);
         prefetch_tmap(&tM);
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) mbar_init(&pp.bars[s], 1);
         fence_mbar_init();
+        pc->item = blockIdx.x;
+        pc->t = 0;
+        pc->kk = 0;
+        pc->set(P);
+        for (int s = 0; s < S - 1 && pc->valid; ++s) {
+            issue<FORM>(P, *pc, smem, pp.bars, s, &tU, &tE, &tP, &tM);
+            pc->next(P);
+        }
     }
     __syncthreads();
-    // producer cursor, S-1 tasks ahead; lives in shared memory (thread 0 only)
-    TaskIt& pit = *reinterpret_cast<TaskIt*>(smem + OFF_PIT);
-    if (threadIdx.x == 0) {
-        pit = it;
-        for (int s = 0; s < S - 1 && pit.valid; ++s) {
-            issue(P, pit, smem, bars, s, &tU, &tE, &tP, &tM);
-            pit.next(P);
-        }
-    }
 
-    double Bc[4][3], Ec = 0.0, top[4][3], ucar[3];
+    double BA[4][3], BB[4][3], EA = 0.0, EB = 0.0, top[4][3], ucar[3] = {0.0, 0.0, 0.0};
     double rsq = 0.0;
     unsigned bad = 0;
-    long long q = 0;
-    for (; it.valid; it.next(P), ++q) {
-        const int st = (int)(q % S);
-        mbar_wait(&bars[st], (uint32_t)((q / S) & 1));
-        const unsigned char* sb = smem + st * STAGE_BYTES;
-        const double* su = reinterpret_cast<const double*>(sb + OFF_U);
-        const double* se = reinterpret_cast<const double*>(sb + OFF_E);
-        const int kc = it.kc();
-        const int i = it.t * 32 + l;
-        const int j = it.s * W - 1 + w;
+    for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
+        const int s = item % P.nstrips;
+        const int ka = g.kb + (item / P.nstrips) * P.chunk;
+        const int kb = min(ka + P.chunk, g.ke);
+        for (int t = 0; t < P.ntx; ++t) {
+            Tile T;
+            T.t = t;
+            T.i = t * 32 + l;
+            T.j = s * W - 1 + w;
+            T.upd = w >= 1 && T.i < g.nx && T.j < g.ny;
+            const bool cxy = T.i <= g.nx - 2 && T.j >= 0 && T.j <= g.ny - 2;
+            T.escale = cxy ? P.e_scale : 0.0;
+            const int ends = (T.i == 0 || T.i == g.nx - 1) + (T.j == 0 || T.j == g.ny - 1);
+            T.invv_xy = P.inv_base * (double)(1 << ends);
+            T.node0 = (long long)max(T.j, 0) * g.px + T.i;
+            T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + w * 3;
+            T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + w * 3;
 
-        // ---- forward butterflies of node plane kc+1 for cell (i, j)
-        double Bn[4][3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double* r0 = su + (c * UROWS + w) * BOXX + l;
-            const double a = r0[0], b = r0[1], cc = r0[BOXX], d = r0[BOXX + 1];
-            const double A0 = a + b, A1 = a - b, A0n = cc + d, A1n = cc - d;
-            Bn[0][c] = A0 + A0n;
-            Bn[1][c] = A1 + A1n;
-            Bn[2][c] = A0 - A0n;
-            Bn[3][c] = A1 - A1n;
-        }
-        const double* e0 = se + w * BOXX + l;
-        const double En = (e0[0] + e0[1]) + (e0[BOXX] + e0[BOXX + 1]);
-
-        const int kind = it.kk;  // 0 prologue, 1 first cell plane, >= 2 owned node plane
-        double face[4][3];
-        if (kind == 0) {
+            // prologue: butterflies of node plane ka-1
+            mbar_wait(&pp.bars[pp.st], pp.phase);
+            forward(pp.smem + pp.st * STAGE_BYTES, w, l, BA, EA);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    Bc[q4][c] = Bn[q4][c];
-                    top[q4][c] = 0.0;
-                }
-            Ec = En;
-        } else {
-            // z butterflies -> modal coefficients C[s][c], s = sx + 2 sy + 4 sz
-            double C[8][3];
+                for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+            end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
+            advance(pp);
+            // first cell plane ka-1: its top face feeds node plane ka
+            {
+                mbar_wait(&pp.bars[pp.st], pp.phase);
+                const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
+                forward(sb, w, l, BB, EB);
+                double face[4][3];
+                cell(P, BA, EA, BB, EB, ka - 1 >= 0 ? T.escale : 0.0, top, face);
+                end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
+                const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    C[q4][c] = Bc[q4][c] + Bn[q4][c];
-                    C[q4 + 4][c] = Bc[q4][c] - Bn[q4][c];
-                    Bc[q4][c] = Bn[q4][c];
-                }
-            const bool valid = i <= g.nx - 2 && j >= 0 && j <= g.ny - 2 && kc >= 0 && kc <= g.nz - 2;
-            const double ecell = valid ? (Ec + En) * P.e_scale : 0.0;
-            Ec = En;
-#pragma unroll
-            for (int s = 1; s < 8; ++s)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) C[s][c] *= ecell;
-            const double* k = P.kh;
-            double F[8][3];
-            F[0][0] = F[0][1] = F[0][2] = 0.0;
-            F[1][0] = k[0] * C[1][0] + k[1] * C[2][1] + k[2] * C[4][2];
-            F[1][1] = k[3] * C[1][1] + k[4] * C[2][0];
-            F[1][2] = k[5] * C[1][2] + k[6] * C[4][0];
-            F[2][0] = k[7] * C[1][1] + k[8] * C[2][0];
-            F[2][1] = k[9] * C[1][0] + k[10] * C[2][1] + k[11] * C[4][2];
-            F[2][2] = k[12] * C[2][2] + k[13] * C[4][1];
-            F[4][0] = k[14] * C[1][2] + k[15] * C[4][0];
-            F[4][1] = k[16] * C[2][2] + k[17] * C[4][1];
-            F[4][2] = k[18] * C[1][0] + k[19] * C[2][1] + k[20] * C[4][2];
-            F[3][0] = k[21] * C[3][0] + k[22] * C[6][2];
-            F[3][1] = k[23] * C[3][1] + k[24] * C[5][2];
-            F[3][2] = k[25] * C[3][2] + k[26] * C[5][1] + k[27] * C[6][0];
-            F[5][0] = k[28] * C[5][0] + k[29] * C[6][1];
-            F[5][1] = k[30] * C[3][2] + k[31] * C[5][1] + k[32] * C[6][0];
-            F[5][2] = k[33] * C[3][1] + k[34] * C[5][2];
-            F[6][0] = k[35] * C[3][2] + k[36] * C[5][1] + k[37] * C[6][0];
-            F[6][1] = k[38] * C[5][0] + k[39] * C[6][1];
-            F[6][2] = k[40] * C[3][0] + k[41] * C[6][2];
-            F[7][0] = k[42] * C[7][0];
-            F[7][1] = k[43] * C[7][1];
-            F[7][2] = k[44] * C[7][2];
-            // inverse z butterflies: bottom face (node plane kc), top face (kc+1)
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    face[q4][c] = top[q4][c] + (F[q4][c] + F[q4 + 4][c]);
-                    top[q4][c] = F[q4][c] - F[q4 + 4][c];
-                }
-        }
-
-        // inverse y butterflies of the face; row j+1's share goes to warp w+1
-        double Yj[2][3];
-        double* sYw = sY + ((size_t)(q & 1) * NWARP * 6 * 32);
-        if (kind >= 2) {
-#pragma unroll
-            for (int sx = 0; sx < 2; ++sx)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    Yj[sx][c] = face[sx][c] + face[sx + 2][c];
-                    sYw[(w * 6 + sx * 3 + c) * 32 + l] = face[sx][c] - face[sx + 2][c];
-                }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && pit.valid) {
-            issue(P, pit, smem, bars, (int)((q + S - 1) % S), &tU, &tE, &tP, &tM);
-            pit.next(P);
-        }
-        if (kind >= 2) {
-            // edge sums, inverse x butterflies, node assembly
-            double Xi[3], Xn[3];
-            if (w >= 1) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const double e0v = Yj[0][c] + sYw[((w - 1) * 6 + c) * 32 + l];
-                    const double e1v = Yj[1][c] + sYw[((w - 1) * 6 + 3 + c) * 32 + l];
-                    Xi[c] = e0v + e1v;
-                    Xn[c] = e0v - e1v;
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) Xi[c] = Xn[c] = 0.0;
+                for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
+                advance(pp);
             }
-            const int zi = kc - it.ka;
-            double* xw = sX + ((size_t)(it.t & 1) * LMAX + zi) * NWARP * 3 + w * 3;
-            const double* xr = sX + ((size_t)((it.t + 1) & 1) * LMAX + zi) * NWARP * 3 + w * 3;
-            double acc[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double nb = __shfl_up_sync(0xffffffffu, Xn[c], 1);
-                acc[c] = Xi[c] + (l > 0 ? nb : (it.t > 0 ? xr[c] : 0.0));
+            // owned planes, two per iteration with alternating register roles
+            int kc = ka;
+            for (; kc + 1 < kb; kc += 2) {
+                own_task<FORM>(P, pp, pc, T, kc, kc - ka, BB, EB, BA, EA, top, ucar, rsq, bad, sY, &tU, &tE, &tP,
+                               &tM);
+                own_task<FORM>(P, pp, pc, T, kc + 1, kc + 1 - ka, BA, EA, BB, EB, top, ucar, rsq, bad, sY, &tU,
+                               &tE, &tP, &tM);
             }
-            if (l == 31) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) xw[c] = Xn[c];
-            }
-            if (w >= 1 && i < g.nx && j < g.ny) {
-                const double* sp = reinterpret_cast<const double*>(sb + OFF_P);
-                const unsigned char mk = (sb + OFF_M)[(w - 1) * 32 + l];
-                const double invv = inv_volume_fast(g, P.inv_base, i, j, kc);
-                const long long node = lidx(g, i, j, kc);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const bool pinned = (mk >> c) & 1;
-                    const double f = ((mk & 8) && !pinned) ? P.aux[c * g.Ns + node] : 0.0;
-                    const double r = -acc[c] * invv - f;
-                    double nv;
-                    if (pinned) {
-                        nv = P.form == 3 ? 0.0 : P.aux[c * g.Ns + node];
-                    } else {
-                        rsq += r * r;
-                        const double cu = ucar[c];
-                        if (P.form == 0) {
-                            const double pp = sp[(c * W + (w - 1)) * 32 + l];
-                            nv = 2.0 * cu - pp + P.a * r - P.b * (cu - pp);
-                        } else if (P.form == 1) {
-                            const double pp = sp[(c * W + (w - 1)) * 32 + l];
-                            nv = (2.0 * cu - pp + P.b * cu + P.a * r) * P.inv;
-                        } else if (P.form == 2) {
-                            nv = cu + P.dt * r;
-                        } else {
-                            nv = r;
-                        }
-                    }
-                    bad |= !isfinite(nv);
-                    P.next[c * g.Ns + node] = nv;
-                }
-            }
+            if (kc < kb)
+                own_task<FORM>(P, pp, pc, T, kc, kc - ka, BB, EB, BA, EA, top, ucar, rsq, bad, sY, &tU, &tE, &tP,
+                               &tM);
         }
-        // own node of plane kc+1 feeds next task's update (this stage is only
-        // recycled after the next task's barrier)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ucar[c] = su[(c * UROWS + w) * BOXX + l];
     }
 
     // CTA reduction of r^2 (fixed order) and the non-finite flag
@@ -347,9 +440,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (l == 0) red[w] = rsq;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int k = 0; k < NWARP; ++k) s += red[k];
-        if (P.partials) P.partials[blockIdx.x] = s;
+        double sum = 0.0;
+        for (int k = 0; k < NWARP; ++k) sum += red[k];
+        if (P.partials) P.partials[blockIdx.x] = sum;
     }
     if (bad && l == 0) mark_bad(P.status, P.step);
 }

@@ -111,6 +111,9 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// TMA descriptors of the fused 3D kernel.  No L2 sector promotion: the 34-column
+// U/E boxes start 256 B-aligned and would drag a second 256 B block each, and the
+// 32-byte mask rows a full 256 B block (measured: 1.6x the algorithmic reads).
 int make_tmaps(petto_ctx* ctx) {
     const Geo& g = ctx->g;
     EncodeTiledFn enc = encode_fn();
@@ -122,11 +125,11 @@ int make_tmaps(petto_ctx* ctx) {
     const cuuint32_t one[4] = {1, 1, 1, 1};
     for (int b = 0; b < 3; ++b) {
         if (enc(&ctx->tU[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxU, one,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return fail(ctx, PETTO_ERROR, "tensor map (state) encode failed");
         if (enc(&ctx->tP[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxP, one,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return fail(ctx, PETTO_ERROR, "tensor map (previous) encode failed");
     }
@@ -134,13 +137,13 @@ int make_tmaps(petto_ctx* ctx) {
     const cuuint64_t s3[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8};
     const cuuint32_t boxE[3] = {e3::BOXX, e3::UROWS, 1};
     if (enc(&ctx->tE, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->prop, d3, s3, boxE, one,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return fail(ctx, PETTO_ERROR, "tensor map (modulus) encode failed");
     const cuuint64_t sm[2] = {(cuuint64_t)g.px, (cuuint64_t)g.px * g.ny};
     const cuuint32_t boxM[3] = {32, e3::W, 1};
     if (enc(&ctx->tM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->mask, d3, sm, boxM, one,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return fail(ctx, PETTO_ERROR, "tensor map (mask) encode failed");
     ctx->tmaps = true;
@@ -233,10 +236,16 @@ StepCoef coef(int form, double dt, double theta) {
     return c;
 }
 
-int fast_grid_3d(const petto_ctx* ctx, long long units) {
-    // persistent CTAs (one per SM), but keep z sub-runs >= 8 planes long
-    long long want = std::max(1LL, units / 8);
-    return (int)std::min<long long>(ctx->nsm, want);
+// Work plan of the fused 3D kernel: items = strips x z-chunks, one CTA per SM.
+// Chunks are as few as fill the SMs (each chunk restarts the z stream: two extra
+// planes), at least 8 planes long, at most LMAX.
+void plan_3d(const petto_ctx* ctx, int nstrips, int& chunks, int& grid) {
+    const int nzo = ctx->g.ke - ctx->g.kb;
+    // a single wave: strips x chunks <= SMs (a partial second wave would double the time)
+    chunks = std::max(1, ctx->nsm / nstrips);
+    chunks = std::min(chunks, std::max(1, nzo / 8));
+    chunks = std::max(chunks, (nzo + e3::LMAX - 1) / e3::LMAX);
+    grid = std::min(ctx->nsm, nstrips * chunks);
 }
 
 void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
@@ -282,7 +291,6 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             const double nu = ctx->desc.poisson_ratio;
             P.e_scale = (1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
             P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
-            P.form = k.form;
             P.dt = k.dt;
             P.a = k.a;
             P.b = k.b;
@@ -294,14 +302,22 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             P.step = step;
             P.nsteps = nsteps;
             P.ntx = (g.nx + 31) / 32;
-            P.nzo = g.ke - g.kb;
-            const int nstrips = (g.ny + e3::W - 1) / e3::W;
-            P.units = (long long)nstrips * P.nzo;
-            const int grid = fast_grid_3d(ctx, P.units);
+            P.nstrips = (g.ny + e3::W - 1) / e3::W;
+            int chunks = 0, grid = 0;
+            plan_3d(ctx, P.nstrips, chunks, grid);
+            const int nzo = g.ke - g.kb;
+            P.chunk = (nzo + chunks - 1) / chunks;
+            P.nitems = P.nstrips * ((nzo + P.chunk - 1) / P.chunk);
+            grid = std::min(grid, P.nitems);
             if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
             timing_begin(ctx, ev);
-            e3::k_elastic3d_fast<<<grid, e3::NTHREADS, e3::SMEM_BYTES, ctx->stream>>>(
-                P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM);
+            const int smem = e3::SMEM_BYTES;
+            switch (k.form) {
+                case 0: e3::k_elastic3d_fast<0><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
+                case 1: e3::k_elastic3d_fast<1><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
+                case 2: e3::k_elastic3d_fast<2><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
+                default: e3::k_elastic3d_fast<3><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
+            }
             timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
             ctx->launches++;
             CKL();
@@ -361,7 +377,8 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
     }
     ctx->launches++;
     CKL();
-    if (k.form == 3) {
+    if (k.form == 3 || want_partials) {
+        // zero_constrained then the serial r^2 (residual_norm in threads == 1 order)
         if (ctx->ncons) {
             k_zero_entries<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->ncons, r,
                                                                            ctx->status, step, nsteps);
@@ -372,7 +389,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             ctx->launches++;
         }
         CKL();
-        return PETTO_OK;
+        if (k.form == 3) return PETTO_OK;
     }
     k_update_replica<<<nb, 256, 0, ctx->stream>>>(g, ctx->comps, k.form, ctx->st[cur], ctx->st[prev], r, next, k.dt,
                                                   k.a, k.b, k.inv, ctx->status, step, nsteps);
@@ -507,8 +524,11 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess)
         return cleanup("out of device memory (scalars)");
-    if (cudaFuncSetAttribute(e3::k_elastic3d_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, e3::SMEM_BYTES) !=
-        cudaSuccess)
+    const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (cudaFuncSetAttribute(e3::k_elastic3d_fast<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_fast<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_fast<2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_fast<3>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");

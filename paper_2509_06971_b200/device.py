@@ -104,8 +104,8 @@ def lib():
     """Load (building if stale, when nvcc is present) the sm_100a library."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.stale():
+        path = os.environ.get("PETTO_B200_LIB") or _build.LIB  # A/B variants of the same C-ABI
+        if path == _build.LIB and _build.stale():
             try:
                 path = _build.build()
             except Exception:
