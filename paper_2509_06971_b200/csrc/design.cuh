@@ -421,6 +421,8 @@ inline void design_free(petto_ctx* ctx) {
     cudaFree(ctx->term1);
     cudaFree(ctx->term2);
     cudaFree(ctx->pmax);
+    cudaFree(ctx->count);
+    ctx->count = nullptr;
     ctx->phases = ctx->gc = ctx->scratch1 = ctx->scratch2 = nullptr;
     ctx->term1 = ctx->term2 = ctx->pmax = nullptr;
     ctx->region_dev = nullptr;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -846,6 +847,394 @@ int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_para
     if (s.aborted)
         return fail(ctx, PETTO_ABORT,
                     "numerical abort in 'state' at step " + std::to_string(n) + ": residual norm diverged");
+    return PETTO_OK;
+}
+
+// ---------------------------------------------------------------- design (a19-a26)
+
+// MaterialModel::validate (objectives.hpp:26-33) / ObjectiveWeights::validate (:44-51)
+static int validate_design(petto_ctx* ctx, const petto_material* m, const petto_weights* w) {
+    if (m->nphases < 1 || m->nphases > PETTO_MAX_PHASES)
+        return fail(ctx, PETTO_INVALID, "material: one property value per phase required");
+    for (int i = 0; i < m->nphases; ++i)
+        if (!(m->properties[i] > 0.0)) return fail(ctx, PETTO_INVALID, "material: properties must be positive");
+    if (m->penalty < 1.0) return fail(ctx, PETTO_INVALID, "material: penalty must be >= 1");
+    if (!(m->void_floor > 0.0)) return fail(ctx, PETTO_INVALID, "material: void floor must be positive");
+    if (w->alpha_compliance < 0 || w->alpha_volume < 0 || w->alpha_unity < 0 || w->alpha_region < 0)
+        return fail(ctx, PETTO_INVALID, "weights: must be non-negative");
+    if (w->alpha_compliance + w->alpha_volume + w->alpha_unity + w->alpha_region <= 0)
+        return fail(ctx, PETTO_INVALID, "weights: at least one weight must be positive");
+    if (w->compliance_sign != 1 && w->compliance_sign != -1)
+        return fail(ctx, PETTO_INVALID, "weights: compliance sign must be +1 or -1");
+    return PETTO_OK;
+}
+
+static DesignP design_params(const petto_ctx* ctx) {
+    DesignP d{};
+    d.np = ctx->mat.nphases;
+    for (int i = 0; i < d.np; ++i) d.props[i] = ctx->mat.properties[i];
+    d.penalty = ctx->mat.penalty;
+    auto ipow = [](double e) {
+        const int ei = (int)e;
+        return (e == (double)ei && ei >= 0 && ei <= 8) ? ei : -1;
+    };
+    d.ipen = ipow(d.penalty);
+    d.ipen1 = ipow(d.penalty - 1.0);
+    d.floor_v = ctx->mat.void_floor;
+    return d;
+}
+
+static double domain_volume(const petto_ctx* ctx) {
+    double v = 1.0;
+    for (int a = 0; a < ctx->g.dim; ++a) v *= ctx->desc.length[a];
+    return v;
+}
+
+// Ordered (REPLICA) or fixed-tree (FAST) sum of n terms into a device scalar.
+static int sum_terms(petto_ctx* ctx, const double* term, long long n, double* dst) {
+    if (ctx->mode == PETTO_MODE_REPLICA) {
+        k_sum_serial<<<1, 32, 0, ctx->stream>>>(term, n, dst);
+        ctx->launches++;
+    } else {
+        const int nb = (int)std::min<long long>(ctx->npartials, blocks_for(n));
+        k_sum_partials<<<nb, 256, 0, ctx->stream>>>(term, n, ctx->partials);
+        k_sum_finish<<<1, 256, 0, ctx->stream>>>(ctx->partials, nb, dst);
+        ctx->launches += 2;
+    }
+    CKL();
+    return PETTO_OK;
+}
+
+static int phase_masses(petto_ctx* ctx, int slot) {
+    const long long owned = owned_nodes(ctx);
+    for (int q = 0; q < ctx->mat.nphases; ++q) {
+        k_term_mass<<<blocks_for(owned), 256, 0, ctx->stream>>>(ctx->g, ctx->phases + q * ctx->g.Ns, ctx->term1);
+        ctx->launches++;
+        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + slot + q)) return rc;
+    }
+    return PETTO_OK;
+}
+
+static int region_sums(petto_ctx* ctx) {
+    if (!ctx->tgt.has_region) return PETTO_OK;
+    const long long n = (long long)ctx->region_nodes.size();
+    const int nb = blocks_for(n);
+    k_region_terms<<<nb, 256, 0, ctx->stream>>>(ctx->g, ctx->region_dev, n, nullptr, ctx->term1);
+    ctx->launches++;
+    if (int rc = sum_terms(ctx, ctx->term1, n, ctx->dscal + DS_RVOL)) return rc;
+    for (int q = 0; q < ctx->mat.nphases; ++q) {
+        k_region_terms<<<nb, 256, 0, ctx->stream>>>(ctx->g, ctx->region_dev, n, ctx->phases + q * ctx->g.Ns,
+                                                    ctx->term1);
+        ctx->launches++;
+        if (int rc = sum_terms(ctx, ctx->term1, n, ctx->dscal + DS_RACC + q)) return rc;
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_set_design(petto_ctx* ctx, const petto_material* m, const petto_targets* t, const petto_weights* w) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = validate_design(ctx, m, w)) return rc;
+    if (t->has_region && t->nregion <= 0)
+        return fail(ctx, PETTO_INVALID, "region_objective: region mask covers no nodes");
+    const Geo& g = ctx->g;
+    ctx->mat = *m;
+    ctx->tgt = *t;
+    ctx->wts = *w;
+    ctx->region_nodes.assign(t->region_nodes, t->region_nodes + (t->has_region ? t->nregion : 0));
+    ctx->tgt.region_nodes = nullptr;
+    design_free(ctx);
+    const size_t P = (size_t)m->nphases;
+    const long long owned = owned_nodes(ctx);
+    CK(cudaMalloc(&ctx->phases, sizeof(double) * P * g.Ns));
+    CK(cudaMalloc(&ctx->gc, sizeof(double) * P * g.Ns));
+    CK(cudaMalloc(&ctx->scratch1, sizeof(double) * g.Ns));
+    CK(cudaMalloc(&ctx->term1, sizeof(double) * std::max<long long>(owned, (long long)ctx->region_nodes.size() + 1)));
+    CK(cudaMalloc(&ctx->term2, sizeof(double) * owned));
+    CK(cudaMalloc(&ctx->pmax, sizeof(double) * 8 * ctx->npartials));
+    CK(cudaMalloc(&ctx->count, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(ctx->phases, 0, sizeof(double) * P * g.Ns, ctx->stream));
+    CK(cudaMemsetAsync(ctx->gc, 0, sizeof(double) * P * g.Ns, ctx->stream));
+    CK(cudaMemsetAsync(ctx->scratch1, 0, sizeof(double) * g.Ns, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dscal, 0, sizeof(double) * 256, ctx->stream));
+    std::vector<unsigned char> mask((size_t)g.Ns, 0);
+    const long long plane = (long long)g.nx * g.ny;
+    for (int64_t node : ctx->region_nodes) {
+        if (node < 0 || node >= global_nodes(ctx)) return fail(ctx, PETTO_INVALID, "region node outside the grid");
+        const int k = (int)(node / plane);
+        if (k < g.ks0 || k >= g.ks0 + g.nzs) continue;
+        const long long r = node - (long long)k * plane;
+        const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
+        mask[lidx(g, i, j, k)] = 1;
+    }
+    CK(cudaMalloc(&ctx->region_mask, (size_t)g.Ns));
+    CK(cudaMemcpyAsync(ctx->region_mask, mask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
+    if (!ctx->region_nodes.empty()) {
+        // region sums run over this rank's owned planes only (list order kept)
+        std::vector<long long> own;
+        for (int64_t node : ctx->region_nodes) {
+            const int k = (int)(node / plane);
+            if (k >= g.kb && k < g.ke) own.push_back(node);
+        }
+        ctx->region_nodes.assign(own.begin(), own.end());
+        CK(cudaMalloc(&ctx->region_dev, sizeof(long long) * std::max<size_t>(own.size(), 1)));
+        if (!own.empty())
+            CK(cudaMemcpyAsync(ctx->region_dev, own.data(), sizeof(long long) * own.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->design_set = true;
+    return PETTO_OK;
+}
+
+int petto_dev_set_phases(petto_ctx* ctx, const double* phases) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (int rc = upload(ctx, ctx->phases, phases, ctx->mat.nphases)) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int petto_dev_get_phases(petto_ctx* ctx, double* phases) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (int rc = download(ctx, phases, ctx->phases, ctx->mat.nphases)) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
+int petto_dev_interpolate(petto_ctx* ctx, double* property_out) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    const long long n = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nzs;
+    k_interpolate<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->g, design_params(ctx), ctx->phases, ctx->prop);
+    ctx->launches++;
+    CKL();
+    ctx->prop_node0_valid = false;
+    if (property_out) {
+        if (int rc = download(ctx, property_out, ctx->prop, 1)) return rc;
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_design_update(petto_ctx* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
+    const Geo& g = ctx->g;
+    const DesignP d = design_params(ctx);
+    if (int rc = phase_masses(ctx, DS_MASS)) return rc;  // volume_fractions of the pre-update design
+    if (int rc = region_sums(ctx)) return rc;
+    const double nu = ctx->mat.poisson_ratio;
+    const double ctr = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double cec = 1.0 / (1.0 + nu);
+    const long long owned = owned_nodes(ctx);
+    const int nb = (int)std::min<long long>(ctx->npartials, blocks_for(owned));
+    k_sens_gc<<<nb, 256, 0, ctx->stream>>>(g, d, ctx->mat.kind, ctr, cec, ctx->phases, ctx->st[ctx->cur], ctx->gc,
+                                          ctx->pmax);
+    UpdateScal u{};
+    u.inv_vol = 1.0 / domain_volume(ctx);
+    for (int q = 0; q < d.np; ++q) {
+        u.fractions[q] = ctx->tgt.fractions[q];
+        u.region_fractions[q] = ctx->tgt.region_fractions[q];
+    }
+    u.has_region = ctx->tgt.has_region;
+    u.alpha_c = ctx->wts.alpha_compliance;
+    u.alpha_v = ctx->wts.alpha_volume;
+    u.alpha_u = ctx->wts.alpha_unity;
+    u.alpha_r = ctx->wts.alpha_region;
+    u.normalize = ctx->wts.normalize_compliance;
+    u.sign = ctx->wts.compliance_sign;
+    k_design_scalars<<<1, 32, 0, ctx->stream>>>(d.np, u, ctx->dscal, ctx->pmax, nb);
+    k_design_update<<<blocks_for(owned), 256, 0, ctx->stream>>>(g, d.np, u, ctx->dscal, ctx->gc, ctx->region_mask,
+                                                               ctx->phases);
+    ctx->launches += 3;
+    CKL();
+    return PETTO_OK;
+}
+
+int petto_dev_ch_step(petto_ctx* ctx, const petto_ch_params* p, petto_ch_stats* stats) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    // CahnHilliardParams::validate (phase_field.hpp:17-21)
+    if (!(p->mobility > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: mobility must be positive");
+    if (!(p->gamma > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: gamma must be positive");
+    if (!(p->dt > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: dt must be positive");
+    const Geo& g = ctx->g;
+    const long long owned = owned_nodes(ctx);
+    const int nb = blocks_for(owned);
+    const double step = p->dt * p->mobility;
+    for (int q = 0; q < ctx->mat.nphases; ++q) {
+        double* phi = ctx->phases + q * g.Ns;
+        k_term_mass<<<nb, 256, 0, ctx->stream>>>(g, phi, ctx->term1);
+        ctx->launches++;
+        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q)) return rc;
+        k_chem_potential<<<nb, 256, 0, ctx->stream>>>(g, phi, p->gamma, ctx->scratch1);
+        k_ch_update<<<nb, 256, 0, ctx->stream>>>(g, ctx->scratch1, step, phi, ctx->term1);
+        ctx->launches += 2;
+        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q + 1)) return rc;
+        k_ch_clamp<<<nb, 256, 0, ctx->stream>>>(g, phi, ctx->term1, &ctx->status->flags);
+        ctx->launches++;
+        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q + 2)) return rc;
+    }
+    CKL();
+    if (stats) {
+        double h[3 * PETTO_MAX_PHASES];
+        CK(cudaMemcpyAsync(h, ctx->dscal + DS_CH, sizeof(double) * 3 * ctx->mat.nphases, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int q = 0; q < ctx->mat.nphases; ++q) {
+            stats[q].mass_before = h[3 * q];
+            stats[q].mass_preclamp = h[3 * q + 1];
+            stats[q].mass_postclamp = h[3 * q + 2];
+        }
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_objectives(petto_ctx* ctx, petto_report* rep, double* separation) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
+    const Geo& g = ctx->g;
+    const int np = ctx->mat.nphases;
+    const long long owned = owned_nodes(ctx);
+    const double nu = ctx->mat.poisson_ratio;
+    const double cl = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double cm = 1.0 / (2.0 * (1.0 + nu));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(unsigned long long), ctx->stream));
+    k_objective_terms<<<blocks_for(owned), 256, 0, ctx->stream>>>(g, design_params(ctx), ctx->mat.kind, cl, cm,
+                                                                 ctx->phases, ctx->st[ctx->cur], ctx->term1,
+                                                                 ctx->term2, ctx->count);
+    ctx->launches++;
+    CKL();
+    if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_OBJ)) return rc;
+    if (int rc = sum_terms(ctx, ctx->term2, owned, ctx->dscal + DS_OBJ + 1)) return rc;
+    if (int rc = phase_masses(ctx, DS_TMP)) return rc;
+    if (int rc = region_sums(ctx)) return rc;
+    double h[DS_COUNT];
+    unsigned long long cnt = 0;
+    CK(cudaMemcpyAsync(h, ctx->dscal, sizeof(double) * DS_COUNT, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&cnt, ctx->count, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    // evaluate_objectives (objectives.hpp:304-320), scalar parts on the host
+    const double inv_vol = 1.0 / domain_volume(ctx);
+    petto_report r{};
+    r.compliance = h[DS_OBJ];
+    r.unity = h[DS_OBJ + 1];
+    double jv = 0.0;
+    for (int q = 0; q < np; ++q) {
+        r.volume_fractions[q] = h[DS_TMP + q] * inv_vol;
+        const double dd = r.volume_fractions[q] - ctx->tgt.fractions[q];
+        jv += dd * dd;
+    }
+    r.volume = jv;
+    r.region = 0.0;
+    if (ctx->tgt.has_region) {
+        double jr = 0.0;
+        for (int q = 0; q < np; ++q) {
+            const double dd = h[DS_RACC + q] / h[DS_RVOL] - ctx->tgt.region_fractions[q];
+            jr += dd * dd;
+        }
+        r.region = jr;
+    }
+    if (rep) *rep = r;
+    if (separation) *separation = (double)cnt / (double)global_nodes(ctx);
+    return PETTO_OK;
+}
+
+// run() (optimizer.hpp:120-223): the coupled loop with every field resident in HBM;
+// the host only sees scalars (records, CH mass stats, abort flags).
+int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, void* user,
+                  petto_run_result* result) {
+    CK(cudaSetDevice(ctx->device));
+    // LoopSchedule::validate (optimizer.hpp:23-33)
+    if (int rc = validate_params(ctx, &s->pt)) return rc;
+    if (!(s->ch.mobility > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: mobility must be positive");
+    if (!(s->ch.gamma > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: gamma must be positive");
+    if (!(s->ch.dt > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: dt must be positive");
+    if (s->max_loops < 1) return fail(ctx, PETTO_INVALID, "schedule: max_loops must be >= 1");
+    if (!(s->convergence_tol > 0.0))
+        return fail(ctx, PETTO_INVALID, "schedule: convergence tolerance must be positive");
+    if (s->convergence_window < 2) return fail(ctx, PETTO_INVALID, "schedule: convergence window must be >= 2");
+    if (s->report_every < 1) return fail(ctx, PETTO_INVALID, "schedule: report_every must be >= 1");
+    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (int rc = validate_design(ctx, &ctx->mat, &ctx->wts)) return rc;
+    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
+
+    petto_run_result res{};
+    // operator construction on the initial design (optimizer.hpp:131-138)
+    if (int rc = petto_dev_interpolate(ctx, nullptr)) return rc;
+    if (int rc = petto_dev_init_operator(ctx)) return rc;
+    std::vector<double> comp_hist;
+    const auto t0 = std::chrono::steady_clock::now();
+    res.termination = 1;
+    std::vector<petto_ch_stats> chs(ctx->mat.nphases);
+    for (long loop = 1; loop <= s->max_loops; ++loop) {
+        res.loops = loop;
+        if (int rc = petto_dev_interpolate(ctx, nullptr)) return rc;
+        int64_t astep = 0;
+        int rc = petto_dev_hybrid_solve(ctx, &s->pt, &astep);
+        if (rc == PETTO_ABORT) {
+            res.termination = 2;
+            std::snprintf(res.abort_detail, sizeof res.abort_detail, "loop %ld: %s", loop, ctx->err.c_str());
+            break;
+        }
+        if (rc) return rc;
+        res.apt_steps += s->pt.n_apt;
+        res.pt_steps += s->pt.n_pt;
+        if ((rc = petto_dev_design_update(ctx))) return rc;
+        ++res.design_updates;
+        CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
+        if ((rc = petto_dev_ch_step(ctx, &s->ch, chs.data()))) return rc;
+        ++res.ch_steps;
+        for (const petto_ch_stats& st : chs) res.clamp_mass_drift += std::abs(st.mass_postclamp - st.mass_preclamp);
+        if ((rc = read_status(ctx))) return rc;
+        if (ctx->status_h->flags & 4u) {
+            res.termination = 2;
+            std::snprintf(res.abort_detail, sizeof res.abort_detail,
+                          "loop %ld: numerical abort in 'phi' at step %ld: design field turned non-finite", loop,
+                          loop);
+            break;
+        }
+        if (loop % s->report_every == 0 || loop == 1 || loop == s->max_loops) {
+            petto_record rec{};
+            petto_report rep{};
+            double sep = 0.0;
+            if ((rc = petto_dev_objectives(ctx, &rep, &sep))) return rc;
+            rec.loop = loop;
+            rec.apt_steps = res.apt_steps;
+            rec.pt_steps = res.pt_steps;
+            rec.compliance = rep.compliance;
+            rec.volume = rep.volume;
+            rec.unity = rep.unity;
+            rec.region = rep.region;
+            for (int q = 0; q < ctx->mat.nphases; ++q) rec.volume_fractions[q] = rep.volume_fractions[q];
+            // the operator sees the property of the updated design (optimizer.hpp:157-162)
+            if ((rc = petto_dev_interpolate(ctx, nullptr))) return rc;
+            if ((rc = petto_dev_residual(ctx, nullptr, &rec.r_pde))) return rc;
+            rec.separation = sep;
+            rec.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            comp_hist.push_back(rec.compliance);
+            if (cb) cb(&rec, user);
+            // converged() (optimizer.hpp:170-181)
+            const int w = s->convergence_window;
+            if ((int)comp_hist.size() >= w) {
+                double lo = comp_hist.back(), hi = lo;
+                for (int i = 0; i < w; ++i) {
+                    const double v = comp_hist[comp_hist.size() - 1 - i];
+                    lo = std::min(lo, v);
+                    hi = std::max(hi, v);
+                }
+                const double scale = std::max(std::abs(hi), 1e-300);
+                if ((hi - lo) / scale < s->convergence_tol) {
+                    res.termination = 0;
+                    break;
+                }
+            }
+        }
+    }
+    if (result) *result = res;
     return PETTO_OK;
 }
 

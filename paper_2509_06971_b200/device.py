@@ -259,6 +259,80 @@ class Context:
                                                          C.c_double(target), C.c_long(max_iters), C.byref(st)))
         return st
 
+    # -- design subsystems ----------------------------------------------------
+    def set_design(self, kind, properties, poisson_ratio, penalty, void_floor, fractions, weights,
+                   region_nodes=None, region_fractions=None):
+        m = Material(kind, len(properties), (C.c_double * MAX_PHASES)(*properties), poisson_ratio, penalty,
+                     void_floor)
+        self._region = np.ascontiguousarray(region_nodes if region_nodes is not None else [0], dtype=np.int64)
+        t = Targets((C.c_double * MAX_PHASES)(*fractions), 1 if region_fractions is not None else 0,
+                    (C.c_double * MAX_PHASES)(*(region_fractions or [])),
+                    len(region_nodes) if region_nodes is not None else 0,
+                    self._region.ctypes.data_as(C.POINTER(C.c_int64)))
+        w = Weights(weights.alpha_compliance, weights.alpha_volume, weights.alpha_unity, weights.alpha_region,
+                    1 if weights.normalize_compliance else 0, int(weights.compliance_sign))
+        self.nphases = len(properties)
+        self._check(lib().petto_dev_set_design(self.h, C.byref(m), C.byref(t), C.byref(w)))
+
+    def set_phases(self, phases):
+        self._check(lib().petto_dev_set_phases(self.h, _dp(_f64(phases))))
+
+    def get_phases(self):
+        out = np.zeros(self.nphases * self.N)
+        self._check(lib().petto_dev_get_phases(self.h, _dp(out)))
+        return out
+
+    def interpolate(self, download=True):
+        out = np.zeros(self.N) if download else None
+        self._check(lib().petto_dev_interpolate(self.h, _dp(out) if download else None))
+        return out
+
+    def design_update(self):
+        self._check(lib().petto_dev_design_update(self.h))
+
+    def ch_step(self, mobility, gamma, dt):
+        st = (CHStats * self.nphases)()
+        self._check(lib().petto_dev_ch_step(self.h, C.byref(CHParams(mobility, gamma, dt)), st))
+        return [(s.mass_before, s.mass_preclamp, s.mass_postclamp) for s in st]
+
+    def objectives(self):
+        rep = Report()
+        sep = C.c_double(0.0)
+        self._check(lib().petto_dev_objectives(self.h, C.byref(rep), C.byref(sep)))
+        return rep, sep.value
+
+    def run(self, sched, callback=None):
+        """run() (optimizer.hpp:120-223); returns (RunResult, [Record])."""
+        s = Schedule(pt_params(sched.pt), CHParams(sched.ch_mobility, sched.ch_gamma, sched.dt_ch),
+                     sched.max_loops, sched.convergence_tol, sched.convergence_window, sched.report_every)
+        records = []
+
+        def _cb(rec, _user):
+            r = rec.contents
+            copy = Record()
+            C.pointer(copy)[0] = r
+            records.append(copy)
+            if callback:
+                callback(copy)
+
+        cb = RECORD_CB(_cb)
+        res = RunResult()
+        self._check(lib().petto_dev_run(self.h, C.byref(s), cb, None, C.byref(res)))
+        return res, records
+
+    @staticmethod
+    def from_problem(prob, mode=MODE_FAST, device=0, k_range=None):
+        """Upload a problem.Problem (build_problem's product) as run() expects it."""
+        ctx = Context(prob.grid, prob.physics, prob.poisson_ratio, mode, device, k_range)
+        ctx.set_constraints(prob.cons_entry, prob.cons_value)
+        ctx.set_source(prob.source)
+        ctx.set_design(prob.physics, prob.properties, prob.poisson_ratio, prob.penalty, prob.void_floor,
+                       prob.fractions, prob.weights, prob.region_nodes if prob.has_region else None,
+                       prob.region_fractions)
+        ctx.set_phases(prob.initial_phases)
+        ctx.set_state(prob.initial_state, prob.initial_state)
+        return ctx
+
     # -- instrumentation -------------------------------------------------------
     def stream(self):
         return lib().petto_dev_stream(self.h)
