@@ -166,6 +166,10 @@ int petto_dev_set_source(petto_ctx* ctx, const double* source);
 /* Property field: conductivity (heat) or Young's modulus (elasticity, stored
  * as Lame mu = E/(2(1+nu)) like update_lame, state_solver.hpp:129-142). */
 int petto_dev_set_property(petto_ctx* ctx, const double* property);
+/* Elasticity from the Lame pair the reference's ElasticityOperator takes
+ * (ElasticMaterialField, state_solver.hpp:106-110, 292-297): mu drives the
+ * residual, lambda only the positivity check and the operator's nu. */
+int petto_dev_set_lame(petto_ctx* ctx, const double* lambda, const double* mu);
 /* ElasticityOperator constructor semantics (state_solver.hpp:292-310): checks
  * the Lame fields are positive, derives nu from node 0 and builds the unit-cell
  * stiffness.  Heat: validates nothing (kappa is checked per residual). */

@@ -47,6 +47,9 @@ struct petto_ctx {
 
     double prop_node0 = 0.0;       // property at global node 0 (operator nu, :299-301)
     bool prop_node0_valid = false;
+    bool prop_is_mu = false;       // elasticity property holds Lame mu (set_lame) instead of E
+    bool lame_bad = false;
+    double lame0[2] = {0.0, 0.0};  // (lambda, mu) at node 0 when set by set_lame
 
     double* partials = nullptr;
     int npartials = 0;

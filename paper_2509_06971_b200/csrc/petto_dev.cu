@@ -290,7 +290,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             P.g = g;
             for (int i = 0; i < 45; ++i) P.kh[i] = ctx->kh[i];
             const double nu = ctx->desc.poisson_ratio;
-            P.e_scale = (1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
+            P.e_scale = (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
             P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
             P.dt = k.dt;
             P.a = k.a;
@@ -342,7 +342,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
         P.src_uniform = ctx->src_value;
         for (int i = 0; i < 10 && i < (int)ctx->kh.size(); ++i) P.kh[i] = ctx->kh[i];
         const double nu = ctx->desc.poisson_ratio;
-        P.e_scale = (1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 4.0);
+        P.e_scale = (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 4.0);
         P.inv_base = g.dim == 3 ? 1.0 / (g.h[0] * g.h[1] * g.h[2]) : 1.0 / (g.h[0] * g.h[1]);
         P.partials = partials;
         P.status = ctx->status;
@@ -367,7 +367,8 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
     const int nb = blocks_for(owned);
     double* r = k.form == 3 ? next : ctx->r;
     if (ctx->desc.physics == 1) {
-        const double cm = 1.0 / (2.0 * (1.0 + ctx->desc.poisson_ratio));
+        // mu per corner: the stored Lame field, or cm * E as update_lame forms it
+        const double cm = ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + ctx->desc.poisson_ratio));
         k_elastic_residual_replica<<<nb, 256, 0, ctx->stream>>>(g, ctx->st[cur], ctx->prop, cm, ctx->src,
                                                                 ctx->Kdev, 2.0 * (1.0 + ctx->nu_op) / (1 << g.dim),
                                                                 r, ctx->status, step, nsteps);
@@ -680,6 +681,29 @@ int petto_dev_set_property(petto_ctx* ctx, const double* property) {
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->prop_node0 = property[0];
     ctx->prop_node0_valid = true;
+    ctx->prop_is_mu = false;
+    return PETTO_OK;
+}
+
+int petto_dev_set_lame(petto_ctx* ctx, const double* lambda, const double* mu) {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->desc.physics != 1) return fail(ctx, PETTO_INVALID, "set_lame: not an elasticity context");
+    // positivity of both Lame fields (state_solver.hpp:295-297), lambda staged in the residual scratch
+    if (int rc = upload(ctx, ctx->r, lambda, 1)) return rc;
+    if (int rc = upload(ctx, ctx->prop, mu, 1)) return rc;
+    CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
+    k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->r, 1.0, 1.0,
+                                                                            &ctx->status->flags);
+    k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->prop, 1.0, 1.0,
+                                                                            &ctx->status->flags);
+    ctx->launches += 2;
+    CKL();
+    if (int rc = read_status(ctx)) return rc;
+    ctx->lame_bad = (ctx->status_h->flags & 1u) != 0;
+    ctx->lame0[0] = lambda[0];
+    ctx->lame0[1] = mu[0];
+    ctx->prop_is_mu = true;
+    ctx->prop_node0_valid = true;
     return PETTO_OK;
 }
 
@@ -692,20 +716,29 @@ int petto_dev_init_operator(petto_ctx* ctx) {
     const double nu = ctx->desc.poisson_ratio;
     const double cl = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     const double cm = 1.0 / (2.0 * (1.0 + nu));
-    CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
-    k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->prop, cl, cm,
-                                                                            &ctx->status->flags);
-    ctx->launches++;
-    CKL();
-    if (int rc = read_status(ctx)) return rc;
-    if (ctx->status_h->flags & 1u) return fail(ctx, PETTO_INVALID, "elasticity: Lame fields must be positive");
-    // nu from node 0's Lame pair (state_solver.hpp:299-301)
-    double e0 = ctx->prop_node0;
-    if (!ctx->prop_node0_valid) {
-        if (ctx->g.kb != 0) return fail(ctx, PETTO_INVALID, "node 0 property unknown on this rank");
-        CK(cudaMemcpy(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), sizeof(double), cudaMemcpyDeviceToHost));
+    double l0, m0;
+    if (ctx->prop_is_mu) {
+        if (ctx->lame_bad) return fail(ctx, PETTO_INVALID, "elasticity: Lame fields must be positive");
+        l0 = ctx->lame0[0];
+        m0 = ctx->lame0[1];
+    } else {
+        CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
+        k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->prop, cl, cm,
+                                                                                &ctx->status->flags);
+        ctx->launches++;
+        CKL();
+        if (int rc = read_status(ctx)) return rc;
+        if (ctx->status_h->flags & 1u) return fail(ctx, PETTO_INVALID, "elasticity: Lame fields must be positive");
+        // Lame pair of node 0 as make_lame / update_lame store it
+        double e0 = ctx->prop_node0;
+        if (!ctx->prop_node0_valid) {
+            if (ctx->g.kb != 0) return fail(ctx, PETTO_INVALID, "node 0 property unknown on this rank");
+            CK(cudaMemcpy(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        l0 = cl * e0;
+        m0 = cm * e0;
     }
-    const double l0 = cl * e0, m0 = cm * e0;
+    // nu from node 0's Lame pair (state_solver.hpp:299-301)
     ctx->nu_op = l0 / (2.0 * (l0 + m0));
     ctx->K = unit_cell_stiffness(ctx->g.dim, ctx->g.h, ctx->nu_op);
     try {
@@ -1010,6 +1043,7 @@ int petto_dev_interpolate(petto_ctx* ctx, double* property_out) {
     ctx->launches++;
     CKL();
     ctx->prop_node0_valid = false;
+    ctx->prop_is_mu = false;
     if (property_out) {
         if (int rc = download(ctx, property_out, ctx->prop, 1)) return rc;
         CK(cudaStreamSynchronize(ctx->stream));

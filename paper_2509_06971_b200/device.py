@@ -131,7 +131,7 @@ def lib():
 EXPORTED = [
     "petto_dev_version", "petto_dev_device_count", "petto_dev_create", "petto_dev_destroy",
     "petto_dev_last_error", "petto_dev_stream", "petto_dev_set_mode", "petto_dev_set_constraints",
-    "petto_dev_set_source", "petto_dev_set_property", "petto_dev_init_operator", "petto_dev_set_state",
+    "petto_dev_set_source", "petto_dev_set_property", "petto_dev_set_lame", "petto_dev_init_operator", "petto_dev_set_state",
     "petto_dev_get_state", "petto_dev_residual", "petto_dev_hybrid_solve", "petto_dev_iterate_to_tolerance",
     "petto_dev_set_design", "petto_dev_set_phases", "petto_dev_get_phases", "petto_dev_interpolate",
     "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
@@ -228,6 +228,9 @@ class Context:
     def set_property(self, prop):
         self._check(lib().petto_dev_set_property(self.h, _dp(_f64(prop))))
 
+    def set_lame(self, lam, mu):
+        self._check(lib().petto_dev_set_lame(self.h, _dp(_f64(lam)), _dp(_f64(mu))))
+
     def init_operator(self):
         self._check(lib().petto_dev_init_operator(self.h))
 
@@ -236,9 +239,11 @@ class Context:
         p = _f64(prev) if prev is not None else c
         self._check(lib().petto_dev_set_state(self.h, _dp(c), _dp(p)))
 
-    def get_state(self):
-        c = np.zeros(self.comps * self.N)
-        p = np.zeros(self.comps * self.N)
+    def get_state(self, out_cur=None, out_prev=None):
+        """Download the history; pass (pinned) arrays to avoid allocating."""
+        c = out_cur if out_cur is not None else np.zeros(self.comps * self.N)
+        p = out_prev if out_prev is not None else np.zeros(self.comps * self.N)
+        assert c.dtype == np.float64 and c.flags.c_contiguous and p.dtype == np.float64 and p.flags.c_contiguous
         self._check(lib().petto_dev_get_state(self.h, _dp(c), _dp(p)))
         return c, p
 

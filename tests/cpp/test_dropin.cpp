@@ -1,0 +1,138 @@
+// test_dropin.cpp -- the reference's own C++ API with the B200 drop-in.
+//
+// Built against the reference headers/sources (tests/cpp/Makefile); the same
+// problem goes through petto::run (CPU reference) and petto::dev::run (B200), and
+// through hybrid_solve / iterate_to_tolerance with the reference's operator types.
+// Prints one line per check and exits non-zero on failure.
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+#include <string>
+
+#include "petto/config_io.hpp"
+#include "petto/engine.hpp"
+#include "petto/parallel.hpp"
+#include "petto_dev.hpp"
+
+using namespace petto;
+
+static int failures = 0;
+
+static void expect(bool ok, const std::string& what) {
+    std::printf("%s %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    if (!ok) ++failures;
+}
+
+static double rel(double a, double b) { return std::abs(a - b) / std::max(std::abs(b), 1e-300); }
+
+static ProblemConfig cfg_of(const char* text) {
+    std::istringstream in(text);
+    return parse_config(in, "<test>");
+}
+
+int main() {
+    par::set_threads(1);
+    // 1. run() on a small cantilever3d (replica mode must track the reference closely)
+    const char* c4 =
+        "preset = cantilever3d\nnx = 24\nny = 10\nnz = 10\nlength_x = 2\nlength_y = 1\nlength_z = 1\n"
+        "properties = 1, 1e-6\ntarget_fractions = 0.3, 0.7\nload_count = 1\nload_0_box = 0,0,0.5,0,1,0.5\n"
+        "load_0_direction = 0,0,1\nload_0_magnitude = 1\nmax_loops = 3\nreport_every = 1\nn_apt = 40\nn_pt = 40\n";
+    for (int mode : {PETTO_MODE_REPLICA, PETTO_MODE_FAST}) {
+        const ProblemConfig cfg = cfg_of(c4);
+        const Problem<double> prob = build_problem<double>(cfg);
+        const LoopSchedule sched = build_schedule(cfg, *prob.grid);
+        const OptimizationResult<double> a = run(prob, sched);
+        const OptimizationResult<double> b = dev::run(prob, sched, {}, mode);
+        bool ok = a.history.size() == b.history.size() && a.loops == b.loops;
+        double worst = 0.0;
+        for (size_t i = 0; ok && i < a.history.size(); ++i) {
+            worst = std::max(worst, rel(b.history[i].compliance, a.history[i].compliance));
+            worst = std::max(worst, rel(b.history[i].volume_fractions[0], a.history[i].volume_fractions[0]));
+        }
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "dev::run %s vs run: worst rel diff %.3e", mode ? "replica" : "fast", worst);
+        expect(ok && worst < (mode ? 1e-12 : 1e-9), buf);
+    }
+    // 2. hybrid_solve with the reference's ElasticityOperator inputs (Lame fields)
+    {
+        const Grid g = Grid::make3d(20, 9, 8, 2.0, 1.0, 0.8);
+        BoundarySpec bc;
+        for (int f = 0; f < 6; ++f) bc.face[f] = {CondKind::TractionFree, 0.0, 0};
+        bc.face[XHi] = {CondKind::Dirichlet, 0.0, 0};
+        Field<double> E(g, 1);
+        for (Index i = 0; i < g.num_nodes(); ++i) E.data[i] = 0.2 + 0.8 * std::fmod(0.37 * i, 1.0);
+        const ElasticMaterialField<double> lame = make_lame(E, 0.3);
+        Field<double> loads(g, 3, 0.0);
+        loads.at(2, g.node(0, 4, 4)) = -1.0;
+        PTParams p;
+        p.dt_pt = g.min_spacing() * g.min_spacing() / 8;
+        p.dt_apt = 0.1 * g.min_spacing();
+        p.n_apt = 30;
+        p.n_pt = 10;
+        p.form = AptForm::SemiImplicitDamping;
+        const ElasticityOperator<double> ref_op(g, lame, loads, bc);
+        StateHistory<double> h1(Field<double>(g, 3, 0.0));
+        hybrid_solve(h1, ref_op, p);
+        const dev::ElasticityOperator dev_op(g, lame, loads, bc, PETTO_MODE_REPLICA);
+        StateHistory<double> h2(Field<double>(g, 3, 0.0));
+        dev::hybrid_solve(h2, dev_op, p);
+        expect(h1.current.data == h2.current.data && h1.previous.data == h2.previous.data,
+               "dev::hybrid_solve (replica, Lame input) bit-identical to hybrid_solve");
+        Field<double> r1(g, 3), r2(g, 3);
+        ref_op.residual(h1.current, r1);
+        dev_op.residual(h1.current, r2);
+        expect(r1.data == r2.data, "DeviceOperator::residual bit-identical to ElasticityOperator::residual");
+    }
+    // 3. iterate_to_tolerance on the criterion-1 Poisson box (n = 32)
+    {
+        const Grid g = Grid::make2d(32, 32, 1.0, 1.0);
+        BoundarySpec bc;
+        for (int f = 0; f < 4; ++f) bc.face[f] = {CondKind::Dirichlet, 0.0, 0};
+        Field<double> kappa(g, 1, 1.0), src(g, 1);
+        for (Index j = 0; j < g.n[1]; ++j)
+            for (Index i = 0; i < g.n[0]; ++i)
+                src.at(0, g.node(i, j)) = std::sin(M_PI * g.coord(0, i)) * std::sin(M_PI * g.coord(1, j));
+        const HeatOperator<double> ref_op(g, kappa, src, bc);
+        PTParams p;
+        p.dt_pt = g.min_spacing() * g.min_spacing() / 4;
+        p.dt_apt = g.min_spacing() / 2;
+        Field<double> r0(g, 1);
+        ref_op.residual(Field<double>(g, 1, 0.0), r0);
+        const double target = 1e-8 * residual_norm(r0);
+        StateHistory<double> h1(Field<double>(g, 1, 0.0));
+        const SolveStats s1 = iterate_to_tolerance(h1, ref_op, IterationMode::APT, p, target, 100000);
+        for (int mode : {PETTO_MODE_REPLICA, PETTO_MODE_FAST}) {
+            const dev::HeatOperator dev_op(g, kappa, src, bc, mode);
+            StateHistory<double> h2(Field<double>(g, 1, 0.0));
+            const SolveStats s2 = dev::iterate_to_tolerance(h2, dev_op, IterationMode::APT, p, target, 100000);
+            char buf[160];
+            std::snprintf(buf, sizeof buf, "dev::iterate_to_tolerance %s: %ld vs %ld iterations",
+                          mode ? "replica" : "fast", s2.iterations, s1.iterations);
+            expect(mode ? s2.iterations == s1.iterations && h2.current.data == h1.current.data
+                        : std::labs(s2.iterations - s1.iterations) <= 1,
+                   buf);
+        }
+    }
+    // 4. error behaviour: reckless dt -> NumericalAbort at the first check
+    {
+        const Grid g = Grid::make2d(16, 16, 1.0, 1.0);
+        BoundarySpec bc;
+        for (int f = 0; f < 4; ++f) bc.face[f] = {CondKind::Dirichlet, 0.0, 0};
+        Field<double> kappa(g, 1, 1.0), f(g, 1, 1.0);
+        const dev::HeatOperator op(g, kappa, f, bc);
+        PTParams p;
+        p.dt_pt = 1e6;
+        p.dt_apt = 0.1;
+        p.n_pt = 5000;
+        StateHistory<double> h(Field<double>(g, 1, 0.0));
+        bool caught = false;
+        try {
+            dev::hybrid_solve(h, op, p);
+        } catch (const NumericalAbort& e) {
+            caught = e.step() == 100 && e.field() == "state";
+        }
+        expect(caught, "dev::hybrid_solve raises NumericalAbort(state, 100)");
+    }
+    std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
+    return failures ? 1 : 0;
+}
