@@ -213,6 +213,25 @@ int petto_dev_objectives(petto_ctx* ctx, petto_report* rep, double* separation);
 int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, void* user,
                   petto_run_result* result);
 
+/* ------------------------------------------- slab decomposition */
+
+/* A rank's context is created with petto_grid_desc.k_begin/k_end = its planes of
+ * the outermost axis and receives the GLOBAL host arrays on upload (it keeps its
+ * planes plus one ghost plane per interior face); downloads fill its owned planes.
+ *
+ * Multi-process (one GPU per rank): rank 0 creates a 128-byte NCCL unique id, the
+ * caller broadcasts it, every rank calls petto_dev_comm_init.  From then on the
+ * state solves exchange ghost planes with the +-1 ranks after every step and
+ * all-reduce the residual norms, masses, maxima and objective sums. */
+int petto_dev_comm_unique_id(void* id128);
+int petto_dev_comm_init(petto_ctx* ctx, const void* id128, int rank, int nranks);
+
+/* Single process driving several contexts (several GPUs, or one GPU in tests):
+ * link the contexts of consecutive slabs, then solve them in lock step with
+ * stream-ordered peer copies of the ghost planes. */
+int petto_dev_group_link(petto_ctx** ctxs, int n);
+int petto_dev_group_hybrid_solve(petto_ctx** ctxs, int n, const petto_pt_params* p, int64_t* abort_step);
+
 /* --------------------------------------------------------------- utilities */
 
 /* detail::unit_cell_stiffness (state_solver.hpp:149-237), node-major dofs. */

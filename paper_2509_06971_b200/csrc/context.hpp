@@ -79,6 +79,14 @@ struct petto_ctx {
     unsigned long long* count = nullptr;
     double* dscal = nullptr;       // device scalars for the design kernels
 
+    // slab decomposition: NCCL ranks or a local group of contexts
+    int rank = 0, nranks = 1;
+    void* nccl_comm = nullptr;       // ncclComm_t
+    petto_ctx* nb_lo = nullptr;      // local-group neighbours (planes below / above)
+    petto_ctx* nb_hi = nullptr;
+    cudaEvent_t ev_step = nullptr;   // local group: this context's step finished
+    cudaEvent_t ev_pull = nullptr;   // local group: this context's ghost pulls finished
+
     // instrumentation
     long long launches = 0;
     bool timing = false;

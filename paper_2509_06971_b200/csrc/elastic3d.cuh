@@ -30,18 +30,43 @@
 // (+1 mask byte); PT drops u_{n-1}.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace petto_b200 {
 namespace e3 {
 
-constexpr int W = 7;           // owned node rows per tile
+// Build-time knobs (A/B variants: -DE3_W=11 -DE3_S=4 -DE3_TOP_SMEM=1 ...).
+#ifndef E3_W
+#define E3_W 7
+#endif
+#ifndef E3_S
+#define E3_S 5
+#endif
+#ifndef E3_TOP_SMEM
+#define E3_TOP_SMEM 0
+#endif
+#ifndef E3_DESYNC
+#define E3_DESYNC 0
+#endif
+#ifndef E3_CONST_KH
+#define E3_CONST_KH 0
+#endif
+constexpr int W = E3_W;        // owned node rows per tile
 constexpr int NWARP = W + 1;   // + y-halo warp
 constexpr int NTHREADS = NWARP * 32;
 constexpr int BOXX = 34;       // TMA box width (33 columns used; 16-byte multiple)
 constexpr int UROWS = W + 2;   // rows j0-1 .. j0+W
-constexpr int S = 5;           // pipeline depth
+constexpr int S = E3_S;        // pipeline depth
 constexpr int LMAX = 64;       // longest z chunk (x-halo buffer)
+constexpr bool TOP_SMEM = E3_TOP_SMEM != 0;  // carried top-face sums in shared memory
+// DESYNC: no CTA-wide barrier per task.  Warp w hands its row-(j+1) face shares to
+// warp w+1 through a pairwise named barrier, and each warp releases a TMA stage
+// through an "empty" mbarrier; warps drift apart by up to a task, so the FP64
+// phase of one warp overlaps the load/exchange phase of another.
+constexpr bool DESYNC = E3_DESYNC != 0;
+constexpr int YD = DESYNC ? S : 2;  // depth of the y-exchange ring (>= the drift bound)
 
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
 constexpr int OFF_U = 0;                                    // [3][UROWS][BOXX] f64
@@ -53,12 +78,38 @@ constexpr uint32_t BYTES_UE = 3 * UROWS * BOXX * 8 + UROWS * BOXX * 8;
 constexpr uint32_t BYTES_P = 3 * W * 32 * 8;
 constexpr uint32_t BYTES_M = W * 32;
 
-constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][6][32] f64
-constexpr int OFF_X = OFF_Y + 2 * NWARP * 6 * 32 * 8;       // [2][LMAX][NWARP][3] f64
-constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] mbarriers
-constexpr int OFF_RED = OFF_BAR + S * 8;                    // [NWARP] f64
+constexpr int OFF_Y = S * STAGE_BYTES;                      // [YD][NWARP][6][32] f64
+constexpr int OFF_X = OFF_Y + YD * NWARP * 6 * 32 * 8;      // [2][LMAX][NWARP][3] f64
+constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] full, [S] empty, [W][S] y-ready
+constexpr int OFF_RED = OFF_BAR + (2 * S + W * S) * 8;      // [NWARP] f64
 constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
-constexpr int SMEM_BYTES = OFF_CUR + 64;
+constexpr int OFF_TOP = OFF_CUR + 128;                      // [12][NTHREADS] f64 (TOP_SMEM)
+constexpr int SMEM_BYTES = OFF_TOP + (TOP_SMEM ? 12 * NTHREADS * 8 : 0);
+
+// Carried top-face contributions of the previous cell plane: 12 doubles per
+// thread, in registers or in the thread's own shared-memory column.
+struct TopRegs {
+    double v[4][3];
+    __device__ __forceinline__ double& at(int q, int c) { return v[q][c]; }
+};
+struct TopSmem {
+    double* p;  // this thread's column
+    __device__ __forceinline__ double& at(int q, int c) { return p[(q * 3 + c) * NTHREADS]; }
+};
+using Top = typename std::conditional<TOP_SMEM, TopSmem, TopRegs>::type;
+__device__ __forceinline__ void bind_top(TopRegs&, unsigned char*) {}
+__device__ __forceinline__ void bind_top(TopSmem& t, unsigned char* smem) {
+    t.p = reinterpret_cast<double*>(smem + OFF_TOP) + threadIdx.x;
+}
+
+// Modal stiffness operands: from the kernel parameters (default) or from a
+// __constant__ bank refreshed on the launching stream before each launch.
+__constant__ double c_kh[48];
+#if E3_CONST_KH
+#define KH c_kh
+#else
+#define KH P.kh
+#endif
 
 struct Params {
     Geo g;
@@ -157,8 +208,9 @@ __device__ __forceinline__ void forward(const unsigned char* sb, int w, int l, d
 
 // z butterflies, modal stiffness, inverse z butterflies: bottom face (node plane
 // kc) returned in face (added to the carried top), new top carried out.
+template <bool EMIT>
 __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], double Ec, const double (&Bn)[4][3],
-                                     double En, double escale, double (&top)[4][3], double (&face)[4][3]) {
+                                     double En, double escale, Top& top, double (&Yj)[2][3], double* sYw) {
     const double ec = (Ec + En) * escale;
     // modal coefficients C[s] = E_cell * (z butterfly), s = sx + 2 sy + 4 sz; the
     // modal stiffness decouples into blocks {1,2,4}, {3,5,6}, {7}, evaluated and
@@ -169,66 +221,117 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     const double c10 = Cp(1, 0), c11 = Cp(1, 1), c12 = Cp(1, 2);
     const double c20 = Cp(2, 0), c21 = Cp(2, 1), c22 = Cp(2, 2);
     const double c40 = Cm(0, 0), c41 = Cm(0, 1), c42 = Cm(0, 2);
-    const double F10 = P.kh[0] * c10 + P.kh[1] * c21 + P.kh[2] * c42;
-    const double F11 = P.kh[3] * c11 + P.kh[4] * c20;
-    const double F12 = P.kh[5] * c12 + P.kh[6] * c40;
-    const double F20 = P.kh[7] * c11 + P.kh[8] * c20;
-    const double F21 = P.kh[9] * c10 + P.kh[10] * c21 + P.kh[11] * c42;
-    const double F22 = P.kh[12] * c22 + P.kh[13] * c41;
-    const double F40 = P.kh[14] * c12 + P.kh[15] * c40;
-    const double F41 = P.kh[16] * c22 + P.kh[17] * c41;
-    const double F42 = P.kh[18] * c10 + P.kh[19] * c21 + P.kh[20] * c42;
+    const double F10 = KH[0] * c10 + KH[1] * c21 + KH[2] * c42;
+    const double F11 = KH[3] * c11 + KH[4] * c20;
+    const double F12 = KH[5] * c12 + KH[6] * c40;
+    const double F20 = KH[7] * c11 + KH[8] * c20;
+    const double F21 = KH[9] * c10 + KH[10] * c21 + KH[11] * c42;
+    const double F22 = KH[12] * c22 + KH[13] * c41;
+    const double F40 = KH[14] * c12 + KH[15] * c40;
+    const double F41 = KH[16] * c22 + KH[17] * c41;
+    const double F42 = KH[18] * c10 + KH[19] * c21 + KH[20] * c42;
     // pair (0, 4): mode 0 (rigid translation) carries no force
-    face[0][0] = top[0][0] + F40;
-    face[0][1] = top[0][1] + F41;
-    face[0][2] = top[0][2] + F42;
-    top[0][0] = -F40;
-    top[0][1] = -F41;
-    top[0][2] = -F42;
+    double f0[3];
+    f0[0] = top.at(0, 0) + F40;
+    f0[1] = top.at(0, 1) + F41;
+    f0[2] = top.at(0, 2) + F42;
+    top.at(0, 0) = -F40;
+    top.at(0, 1) = -F41;
+    top.at(0, 2) = -F42;
     // block B: bilinear modes 3 (xy), 5 (xz), 6 (yz)
     const double c30 = Cp(3, 0), c31 = Cp(3, 1), c32 = Cp(3, 2);
     const double c50 = Cm(1, 0), c51 = Cm(1, 1), c52 = Cm(1, 2);
     const double c60 = Cm(2, 0), c61 = Cm(2, 1), c62 = Cm(2, 2);
-    const double F30 = P.kh[21] * c30 + P.kh[22] * c62;
-    const double F31 = P.kh[23] * c31 + P.kh[24] * c52;
-    const double F32 = P.kh[25] * c32 + P.kh[26] * c51 + P.kh[27] * c60;
-    const double F50 = P.kh[28] * c50 + P.kh[29] * c61;
-    const double F51 = P.kh[30] * c32 + P.kh[31] * c51 + P.kh[32] * c60;
-    const double F52 = P.kh[33] * c31 + P.kh[34] * c52;
-    const double F60 = P.kh[35] * c32 + P.kh[36] * c51 + P.kh[37] * c60;
-    const double F61 = P.kh[38] * c50 + P.kh[39] * c61;
-    const double F62 = P.kh[40] * c30 + P.kh[41] * c62;
+    const double F30 = KH[21] * c30 + KH[22] * c62;
+    const double F31 = KH[23] * c31 + KH[24] * c52;
+    const double F32 = KH[25] * c32 + KH[26] * c51 + KH[27] * c60;
+    const double F50 = KH[28] * c50 + KH[29] * c61;
+    const double F51 = KH[30] * c32 + KH[31] * c51 + KH[32] * c60;
+    const double F52 = KH[33] * c31 + KH[34] * c52;
+    const double F60 = KH[35] * c32 + KH[36] * c51 + KH[37] * c60;
+    const double F61 = KH[38] * c50 + KH[39] * c61;
+    const double F62 = KH[40] * c30 + KH[41] * c62;
     // pairs (1, 5) and (2, 6)
-    face[1][0] = top[1][0] + (F10 + F50);
-    face[1][1] = top[1][1] + (F11 + F51);
-    face[1][2] = top[1][2] + (F12 + F52);
-    top[1][0] = F10 - F50;
-    top[1][1] = F11 - F51;
-    top[1][2] = F12 - F52;
-    face[2][0] = top[2][0] + (F20 + F60);
-    face[2][1] = top[2][1] + (F21 + F61);
-    face[2][2] = top[2][2] + (F22 + F62);
-    top[2][0] = F20 - F60;
-    top[2][1] = F21 - F61;
-    top[2][2] = F22 - F62;
-    // block C: trilinear mode 7, pair (3, 7)
+    double f1[3];
+    f1[0] = top.at(1, 0) + (F10 + F50);
+    f1[1] = top.at(1, 1) + (F11 + F51);
+    f1[2] = top.at(1, 2) + (F12 + F52);
+    top.at(1, 0) = F10 - F50;
+    top.at(1, 1) = F11 - F51;
+    top.at(1, 2) = F12 - F52;
+    const double f20 = top.at(2, 0) + (F20 + F60);
+    const double f21 = top.at(2, 1) + (F21 + F61);
+    const double f22 = top.at(2, 2) + (F22 + F62);
+    top.at(2, 0) = F20 - F60;
+    top.at(2, 1) = F21 - F61;
+    top.at(2, 2) = F22 - F62;
+    // inverse y butterflies of the sx = 0 face modes: row j keeps the sum, row j+1
+    // (warp w+1) gets the difference through shared memory
+    if (EMIT) {
+        Yj[0][0] = f0[0] + f20;
+        Yj[0][1] = f0[1] + f21;
+        Yj[0][2] = f0[2] + f22;
+        sYw[0 * 32] = f0[0] - f20;
+        sYw[1 * 32] = f0[1] - f21;
+        sYw[2 * 32] = f0[2] - f22;
+    }
+    // block C: trilinear mode 7, pair (3, 7), then the sx = 1 face modes
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double F7 = P.kh[42 + c] * Cm(3, c);
+        const double F7 = KH[42 + c] * Cm(3, c);
         const double F3 = c == 0 ? F30 : (c == 1 ? F31 : F32);
-        face[3][c] = top[3][c] + (F3 + F7);
-        top[3][c] = F3 - F7;
+        const double f3 = top.at(3, c) + (F3 + F7);
+        top.at(3, c) = F3 - F7;
+        if (EMIT) {
+            Yj[1][c] = f1[c] + f3;
+            sYw[(3 + c) * 32] = f1[c] - f3;
+        }
     }
 }
 
+// Mid-task hand-off (after the y shares are written).  Synchronous mode: one CTA
+// barrier, then the producer refills the stage of the previous task.
 template <int FORM>
 __device__ __forceinline__ void end_task(const Params& P, Pipe& pp, Cursor* pc, const CUtensorMap* tU,
                                          const CUtensorMap* tE, const CUtensorMap* tP, const CUtensorMap* tM) {
+    if (DESYNC) return;
     __syncthreads();
     if (threadIdx.x == 0 && pc->valid) {
         issue<FORM>(P, *pc, pp.smem, pp.bars, pp.st == 0 ? S - 1 : pp.st - 1, tU, tE, tP, tM);
         pc->next(P);
     }
+}
+
+// End of a task (after the warp's last read of the stage).  Desync mode: the warp
+// releases the stage; thread 0 refills the stage of the previous task once every
+// warp has released it.
+template <int FORM>
+__device__ __forceinline__ void release(const Params& P, Pipe& pp, Cursor* pc, const CUtensorMap* tU,
+                                        const CUtensorMap* tE, const CUtensorMap* tP, const CUtensorMap* tM) {
+    if (!DESYNC) return;
+    __syncwarp();
+    uint64_t* empty = pp.bars + S;
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[pp.st]);
+    if (threadIdx.x == 0 && pc->valid) {
+        const int prev = pp.st == 0 ? S - 1 : pp.st - 1;
+        if (pp.q >= 1) mbar_wait(&empty[prev], pp.st == 0 ? pp.phase ^ 1u : pp.phase);
+        issue<FORM>(P, *pc, pp.smem, pp.bars, prev, tU, tE, tP, tM);
+        pc->next(P);
+    }
+}
+
+// The y-ready barriers complete one phase per task, so tasks without a y exchange
+// (prologue, first cell plane) still hand off to keep the phases aligned with the
+// task counter.
+__device__ __forceinline__ void y_handoff(Pipe& pp) {
+    if (!DESYNC) return;
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t* yready = pp.bars + 2 * S;
+    if (w < W) {
+        __syncwarp();
+        if (l == 0) mbar_arrive(&yready[w * S + pp.st]);
+    }
+    if (w > 0) mbar_wait(&yready[(w - 1) * S + pp.st], pp.phase);
 }
 
 __device__ __forceinline__ void advance(Pipe& pp) {
@@ -244,7 +347,7 @@ __device__ __forceinline__ void advance(Pipe& pp) {
 template <int FORM>
 __device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, const Tile& T, int kc, int zi,
                                          const double (&Bc)[4][3], double Ec, double (&Bn)[4][3], double& En,
-                                         double (&top)[4][3], double (&ucar)[3], double& rsq, unsigned& bad,
+                                         Top& top, double (&ucar)[3], double& rsq, unsigned& bad,
                                          double* sY, const CUtensorMap* tU, const CUtensorMap* tE,
                                          const CUtensorMap* tP, const CUtensorMap* tM) {
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -252,29 +355,35 @@ __device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, 
     mbar_wait(&pp.bars[pp.st], pp.phase);
     const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
     forward(sb, w, l, Bn, En);
-    double face[4][3];
-    cell(P, Bc, Ec, Bn, En, kc <= g.nz - 2 ? T.escale : 0.0, top, face);
-    // inverse y butterflies; row j+1's share to warp w+1
-    double* sYw = sY + (pp.q & 1) * (NWARP * 6 * 32);
+    // cell plane kc with the inverse y butterflies: row j's sums in Yj, row j+1's
+    // shares to warp w+1 through shared memory
+    double* sYw = sY + (DESYNC ? pp.st : (pp.q & 1)) * (NWARP * 6 * 32);
     double Yj[2][3];
-#pragma unroll
-    for (int sx = 0; sx < 2; ++sx)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            Yj[sx][c] = face[sx][c] + face[sx + 2][c];
-            sYw[(w * 6 + sx * 3 + c) * 32 + l] = face[sx][c] - face[sx + 2][c];
-        }
+    cell<true>(P, Bc, Ec, Bn, En, kc <= g.nz - 2 ? T.escale : 0.0, top, Yj, sYw + w * 6 * 32 + l);
+    uint64_t* yready = pp.bars + 2 * S;  // [W][S]: warp w's shares of task q ready
+    if (DESYNC && w < W) {
+        __syncwarp();
+        if (l == 0) mbar_arrive(&yready[w * S + pp.st]);
+    }
     end_task<FORM>(P, pp, pc, tU, tE, tP, tM);
     // edge sums (w >= 1), inverse x butterflies, node assembly
-    const double* below = sYw + ((w > 0 ? w - 1 : 0) * 6) * 32 + l;
-    const double wsel = w > 0 ? 1.0 : 0.0;
     double Xi[3], Xn[3];
+    if (w > 0) {  // warp-uniform
+        if (DESYNC) mbar_wait(&yready[(w - 1) * S + pp.st], pp.phase);
+        const double* below = sYw + (w - 1) * 6 * 32 + l;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const double e0v = Yj[0][c] + wsel * below[c * 32];
-        const double e1v = Yj[1][c] + wsel * below[(3 + c) * 32];
-        Xi[c] = e0v + e1v;
-        Xn[c] = e0v - e1v;
+        for (int c = 0; c < 3; ++c) {
+            const double e0v = Yj[0][c] + below[c * 32];
+            const double e1v = Yj[1][c] + below[(3 + c) * 32];
+            Xi[c] = e0v + e1v;
+            Xn[c] = e0v - e1v;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            Xi[c] = Yj[0][c] + Yj[1][c];
+            Xn[c] = Yj[0][c] - Yj[1][c];
+        }
     }
     double acc[3];
     const double* xr = T.xr + zi * (NWARP * 3);
@@ -341,6 +450,7 @@ __device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, 
     const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
 #pragma unroll
     for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
+    release<FORM>(P, pp, pc, tU, tE, tP, tM);
     advance(pp);
 }
 
@@ -362,7 +472,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         prefetch_tmap(&tE);
         prefetch_tmap(&tP);
         prefetch_tmap(&tM);
-        for (int s = 0; s < S; ++s) mbar_init(&pp.bars[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&pp.bars[s], 1);          // full: the producer's expect_tx + TMA bytes
+            mbar_init(&pp.bars[S + s], NWARP);  // empty: one arrival per warp
+        }
+        for (int b = 0; b < W * S; ++b) mbar_init(&pp.bars[2 * S + b], 1);  // y-ready: producer lane 0
         fence_mbar_init();
         pc->item = blockIdx.x;
         pc->t = 0;
@@ -375,7 +489,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
 
-    double BA[4][3], BB[4][3], EA = 0.0, EB = 0.0, top[4][3], ucar[3] = {0.0, 0.0, 0.0};
+    double BA[4][3], BB[4][3], EA = 0.0, EB = 0.0, ucar[3] = {0.0, 0.0, 0.0};
+    Top top;
+    bind_top(top, smem);
     double rsq = 0.0;
     unsigned bad = 0;
     for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
@@ -402,20 +518,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+                for (int c = 0; c < 3; ++c) top.at(q4, c) = 0.0;
             end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
+            y_handoff(pp);
+            release<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
             advance(pp);
             // first cell plane ka-1: its top face feeds node plane ka
             {
                 mbar_wait(&pp.bars[pp.st], pp.phase);
                 const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
                 forward(sb, w, l, BB, EB);
-                double face[4][3];
-                cell(P, BA, EA, BB, EB, ka - 1 >= 0 ? T.escale : 0.0, top, face);
+                double Yj[2][3];
+                cell<false>(P, BA, EA, BB, EB, ka - 1 >= 0 ? T.escale : 0.0, top, Yj, nullptr);
                 end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
                 const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
+                y_handoff(pp);
+                release<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
                 advance(pp);
             }
             // owned planes, two per iteration with alternating register roles

@@ -18,6 +18,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "comm.hpp"
 #include "context.hpp"
 #include "design.cuh"
 #include "elastic3d.cuh"
@@ -311,6 +312,12 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             P.nitems = P.nstrips * ((nzo + P.chunk - 1) / P.chunk);
             grid = std::min(grid, P.nitems);
             if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
+#if E3_CONST_KH
+            // stream-ordered refresh of the constant bank the kernel reads the
+            // modal stiffness from (contexts that share a device serialise here)
+            CK(cudaMemcpyToSymbolAsync(e3::c_kh, P.kh, sizeof(double) * 45, 0, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+#endif
             timing_begin(ctx, ev);
             const int smem = e3::SMEM_BYTES;
             switch (k.form) {
@@ -428,6 +435,78 @@ int require_ready(petto_ctx* ctx) {
     return PETTO_OK;
 }
 
+// ------------------------------------------------------------ slab transport
+
+enum FieldSel { F_STATE = 0, F_PROP = 1, F_PHASES = 2, F_SCRATCH1 = 3 };
+
+double* field_of(petto_ctx* c, FieldSel s, int buf) {
+    switch (s) {
+        case F_STATE: return c->st[buf];
+        case F_PROP: return c->prop;
+        case F_PHASES: return c->phases;
+        default: return c->scratch1;
+    }
+}
+
+int comps_of(const petto_ctx* c, FieldSel s) {
+    return s == F_STATE ? c->comps : (s == F_PHASES ? c->mat.nphases : 1);
+}
+
+int nccl_check(petto_ctx* ctx, ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return PETTO_OK;
+    const char* m = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
+    return fail(ctx, PETTO_ERROR, std::string(what) + ": " + m);
+}
+
+// Ghost planes of `field` from the +-1 ranks (NCCL transport), stream ordered after
+// the kernel that wrote the owned planes.  No-op on a single rank.
+int halo(petto_ctx* ctx, FieldSel s, int buf) {
+    if (!ctx->nccl_comm) return PETTO_OK;
+    NcclApi& N = nccl();
+    const ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+    const Geo& g = ctx->g;
+    double* f = field_of(ctx, s, buf);
+    const size_t plane = (size_t)g.px * g.ny;
+    N.GroupStart();
+    for (int c = 0; c < comps_of(ctx, s); ++c) {
+        double* fc = f + c * g.Ns;
+        if (ctx->rank > 0) {
+            N.Send(fc + lidx(g, 0, 0, g.kb), plane, ncclDouble, ctx->rank - 1, comm, ctx->stream);
+            N.Recv(fc + lidx(g, 0, 0, g.kb - 1), plane, ncclDouble, ctx->rank - 1, comm, ctx->stream);
+        }
+        if (ctx->rank < ctx->nranks - 1) {
+            N.Send(fc + lidx(g, 0, 0, g.ke - 1), plane, ncclDouble, ctx->rank + 1, comm, ctx->stream);
+            N.Recv(fc + lidx(g, 0, 0, g.ke), plane, ncclDouble, ctx->rank + 1, comm, ctx->stream);
+        }
+    }
+    return nccl_check(ctx, N.GroupEnd(), "halo exchange");
+}
+
+// In-place all-reduce of device scalars across the ranks (no-op on one rank).
+int allreduce(petto_ctx* ctx, void* p, size_t n, ncclDataType_t t, ncclRedOp_t op) {
+    if (!ctx->nccl_comm) return PETTO_OK;
+    return nccl_check(ctx, nccl().AllReduce(p, p, n, t, op, static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream),
+                      "all-reduce");
+}
+
+// Local group: pull this context's ghost planes of state buffer `buf` from the
+// neighbours' owned planes once their step has finished.
+int group_pull(petto_ctx* ctx, int buf) {
+    const Geo& g = ctx->g;
+    const size_t bytes = sizeof(double) * (size_t)g.px * g.ny;
+    for (petto_ctx* nb : {ctx->nb_lo, ctx->nb_hi}) {
+        if (!nb) continue;
+        CK(cudaStreamWaitEvent(ctx->stream, nb->ev_step, 0));
+        const int k = nb == ctx->nb_lo ? g.kb - 1 : g.ke;  // ghost plane = neighbour's owned plane
+        for (int c = 0; c < ctx->comps; ++c)
+            CK(cudaMemcpyAsync(ctx->st[buf] + c * g.Ns + lidx(g, 0, 0, k),
+                               nb->st[buf] + c * nb->g.Ns + lidx(nb->g, 0, 0, k), bytes, cudaMemcpyDefault,
+                               ctx->stream));
+    }
+    CK(cudaEventRecord(ctx->ev_pull, ctx->stream));
+    return PETTO_OK;
+}
+
 // kappa > 0 guard of variable_diffusion_into (stencil.hpp:145-157), checked once per
 // call because kappa is constant within a solve.
 int check_kappa(petto_ctx* ctx) {
@@ -540,7 +619,13 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
 
 void petto_dev_destroy(petto_ctx* ctx) {
     if (!ctx) return;
+    cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
+    for (petto_ctx* nb : {ctx->nb_lo, ctx->nb_hi})  // unlink from a local group
+        if (nb) (nb->nb_lo == ctx ? nb->nb_lo : nb->nb_hi) = nullptr;
+    if (ctx->ev_step) cudaEventDestroy(ctx->ev_step);
+    if (ctx->ev_pull) cudaEventDestroy(ctx->ev_pull);
     for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
     cudaFree(ctx->prop);
     cudaFree(ctx->aux);
@@ -786,6 +871,7 @@ int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
         ctx->launches++;
         CKL();
     }
+    if (int rc = allreduce(ctx, &ctx->status->sumsq, 1, ncclDouble, ncclSum)) return rc;
     if (int rc = read_status(ctx)) return rc;
     if (r_pde) *r_pde = std::sqrt(ctx->status_h->sumsq) / (double)global_nodes(ctx);
     if (out) {
@@ -819,11 +905,15 @@ int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* ab
         // next := previous buffer, written in place; then swap (state_solver.hpp:421, 440)
         if (int rc = state_step(ctx, ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
         std::swap(ctx->cur, ctx->prev);
+        if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
     }
     for (long s = 0; s < p->n_pt; ++s) {
         if (int rc = state_step(ctx, kp, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
         std::swap(ctx->cur, ctx->prev);
+        if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
     }
+    // every rank aborts at the same check_finite step
+    if (int rc = allreduce(ctx, &ctx->status->first_bad, 1, ncclInt64, ncclMin)) return rc;
     if (int rc = read_status(ctx)) return rc;
     if (ctx->status_h->first_bad != PETTO_NO_BAD) {
         const long long fb = ctx->status_h->first_bad;
@@ -859,9 +949,20 @@ int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_para
             if (int rc = state_step(ctx, k, b[it % 3], b[(it + 2) % 3], ctx->st[b[(it + 1) % 3]], it + 1, never,
                                     true))
                 return rc;
-            k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status,
-                                                      ctx->mode == PETTO_MODE_FAST ? ctx->partials : nullptr,
-                                                      ctx->npartials_used);
+            if (ctx->nccl_comm) {
+                // global r^2: local sum, all-reduce, then the stop test on every rank
+                if (ctx->mode == PETTO_MODE_FAST) {
+                    k_sum_to<<<1, 256, 0, ctx->stream>>>(ctx->partials, ctx->npartials_used, &ctx->status->sumsq);
+                    ctx->launches++;
+                }
+                if (int rc = allreduce(ctx, &ctx->status->sumsq, 1, ncclDouble, ncclSum)) return rc;
+                k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status, nullptr, 0);
+                if (int rc = halo(ctx, F_STATE, b[(it + 1) % 3])) return rc;
+            } else {
+                k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status,
+                                                          ctx->mode == PETTO_MODE_FAST ? ctx->partials : nullptr,
+                                                          ctx->npartials_used);
+            }
             ctx->launches++;
             CKL();
         }
@@ -1269,6 +1370,113 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
         }
     }
     if (result) *result = res;
+    return PETTO_OK;
+}
+
+// ------------------------------------------------------------ slab decomposition
+
+int petto_dev_comm_unique_id(void* id128) {
+    std::string err;
+    if (!nccl().load(err)) return fail(nullptr, PETTO_ERROR, err);
+    ncclUniqueId id;
+    if (nccl().GetUniqueId(&id) != ncclSuccess) return fail(nullptr, PETTO_ERROR, "ncclGetUniqueId failed");
+    std::memcpy(id128, &id, sizeof(id));
+    return PETTO_OK;
+}
+
+int petto_dev_comm_init(petto_ctx* ctx, const void* id128, int rank, int nranks) {
+    CK(cudaSetDevice(ctx->device));
+    std::string err;
+    if (!nccl().load(err)) return fail(ctx, PETTO_ERROR, err);
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, PETTO_INVALID, "comm: bad rank / size");
+    if ((rank > 0) != (ctx->g.kb > 0) || (rank < nranks - 1) != (ctx->g.ke < ctx->g.nz))
+        return fail(ctx, PETTO_INVALID, "comm: the context's plane range does not match the rank order");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm = nullptr;
+    if (int rc = nccl_check(ctx, nccl().CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank")) return rc;
+    ctx->nccl_comm = comm;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    return PETTO_OK;
+}
+
+int petto_dev_group_link(petto_ctx** c, int n) {
+    for (int i = 0; i < n; ++i) {
+        petto_ctx* x = c[i];
+        petto_ctx* ctx = x;  // error sink of CK()
+        if (i + 1 < n && (x->g.ke != c[i + 1]->g.kb || x->g.nx != c[i + 1]->g.nx || x->g.ny != c[i + 1]->g.ny))
+            return fail(x, PETTO_INVALID, "group: contexts must hold consecutive slabs of one grid");
+        x->nb_lo = i > 0 ? c[i - 1] : nullptr;
+        x->nb_hi = i + 1 < n ? c[i + 1] : nullptr;
+        x->rank = i;
+        x->nranks = n;
+        CK(cudaSetDevice(x->device));
+        if (!x->ev_step) CK(cudaEventCreateWithFlags(&x->ev_step, cudaEventDisableTiming));
+        if (!x->ev_pull) CK(cudaEventCreateWithFlags(&x->ev_pull, cudaEventDisableTiming));
+        CK(cudaEventRecord(x->ev_step, x->stream));
+        CK(cudaEventRecord(x->ev_pull, x->stream));
+        for (petto_ctx* nb : {x->nb_lo, x->nb_hi}) {
+            if (!nb || nb->device == x->device) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, x->device, nb->device);
+            if (can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(nb->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+            }
+        }
+    }
+    return PETTO_OK;
+}
+
+// hybrid_solve over a linked group: every step runs on all slabs, then each slab
+// pulls its ghost planes from its neighbours (stream-ordered, no host sync).
+int petto_dev_group_hybrid_solve(petto_ctx** c, int n, const petto_pt_params* p, int64_t* abort_step) {
+    petto_ctx* ctx = c[0];  // error sink of CK()
+    for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(c[i]->device));
+        if (int rc = validate_params(c[i], p)) return rc;
+        if (int rc = require_ready(c[i])) return rc;
+        if (int rc = check_kappa(c[i])) return rc;
+        if (int rc = reset_status(c[i])) return rc;
+        if (n > 1 && (c[i]->nb_lo != (i ? c[i - 1] : nullptr) || c[i]->nb_hi != (i + 1 < n ? c[i + 1] : nullptr)))
+            return fail(c[i], PETTO_INVALID, "group: call petto_dev_group_link first");
+    }
+    const long long nsteps = p->n_apt + p->n_pt;
+    const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
+    const StepCoef kp = coef(2, p->dt_pt, p->theta);
+    for (long long step = 1; step <= nsteps; ++step) {
+        const StepCoef& k = step <= p->n_apt ? ka : kp;
+        for (int i = 0; i < n; ++i) {
+            petto_ctx* x = c[i];
+            CK(cudaSetDevice(x->device));
+            // the buffer written now was read by the neighbours' pulls of the last step
+            for (petto_ctx* nb : {x->nb_lo, x->nb_hi})
+                if (nb) CK(cudaStreamWaitEvent(x->stream, nb->ev_pull, 0));
+            if (int rc = state_step(x, k, x->cur, x->prev, x->st[x->prev], step, nsteps, false)) return rc;
+            std::swap(x->cur, x->prev);
+            CK(cudaEventRecord(x->ev_step, x->stream));
+        }
+        for (int i = 0; i < n; ++i) {
+            CK(cudaSetDevice(c[i]->device));
+            if (int rc = group_pull(c[i], c[i]->cur)) return rc;
+        }
+    }
+    long long fb = PETTO_NO_BAD;
+    for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(c[i]->device));
+        if (int rc = read_status(c[i])) return rc;
+        fb = std::min(fb, c[i]->status_h->first_bad);
+    }
+    if (fb != PETTO_NO_BAD) {
+        const long long at = std::min(((fb + 99) / 100) * 100, nsteps);
+        for (int i = 0; i < n; ++i)
+            if ((nsteps - at) % 2) std::swap(c[i]->cur, c[i]->prev);
+        if (abort_step) *abort_step = at;
+        return fail(c[0], PETTO_ABORT, "numerical abort in 'state' at step " + std::to_string(at) +
+                                           ": non-finite values (time step too large?)");
+    }
     return PETTO_OK;
 }
 

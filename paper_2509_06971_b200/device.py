@@ -136,8 +136,30 @@ EXPORTED = [
     "petto_dev_set_design", "petto_dev_set_phases", "petto_dev_get_phases", "petto_dev_interpolate",
     "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
     "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
-    "petto_dev_kernel_timing", "petto_dev_kernel_stats",
+    "petto_dev_kernel_timing", "petto_dev_kernel_stats", "petto_dev_comm_unique_id", "petto_dev_comm_init",
+    "petto_dev_group_link", "petto_dev_group_hybrid_solve",
 ]
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (rank 0), to be broadcast by the caller."""
+    buf = (C.c_ubyte * 128)()
+    rc = lib().petto_dev_comm_unique_id(buf)
+    if rc != OK:
+        raise RuntimeError(lib().petto_dev_last_error(None).decode())
+    return bytes(buf)
+
+
+def group_link(ctxs):
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    ctxs[0]._check(lib().petto_dev_group_link(arr, len(ctxs)))
+
+
+def group_hybrid_solve(ctxs, params):
+    """hybrid_solve on a linked group of slab contexts (one process)."""
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    step = C.c_int64(0)
+    ctxs[0]._check(lib().petto_dev_group_hybrid_solve(arr, len(ctxs), C.byref(pt_params(params)), C.byref(step)))
 
 
 def _dp(a):
@@ -337,6 +359,11 @@ class Context:
         ctx.set_phases(prob.initial_phases)
         ctx.set_state(prob.initial_state, prob.initial_state)
         return ctx
+
+    def comm_init(self, uid, rank, nranks):
+        """Join the NCCL communicator of the slab decomposition (one GPU per rank)."""
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        self._check(lib().petto_dev_comm_init(self.h, buf, int(rank), int(nranks)))
 
     # -- instrumentation -------------------------------------------------------
     def stream(self):
