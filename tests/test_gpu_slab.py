@@ -58,6 +58,35 @@ def test_group_equals_single_domain(physics, nranks, mode):
     assert np.array_equal(got_c, want_c) and np.array_equal(got_p, want_p)
 
 
+@pytest.mark.parametrize("mode", [D.MODE_FAST, D.MODE_REPLICA])
+def test_single_rank_nccl_paths(mode):
+    """A one-rank NCCL communicator runs the distributed code paths (halo no-ops,
+    all-reduced norms, device-side stop test after the all-reduce) and must give
+    the same answers as the plain context."""
+    g = P.Grid.make3d(33, 12, 10, 2.0, 1.0, 0.7)
+    comps, prop, src, bc, cur, prev = inputs(g, 1)
+    e, v = P.make_constraints(g, bc, comps)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.2 * h, theta=1.0, n_apt=30, n_pt=10, form=1)
+    outs = []
+    for use_comm in (False, True):
+        ctx = D.Context(g, 1, 0.3, mode)
+        ctx.set_constraints(e, v)
+        ctx.set_source(src)
+        ctx.set_property(prop)
+        ctx.init_operator()
+        if use_comm:
+            ctx.comm_init(D.comm_unique_id(), 0, 1)
+        ctx.set_state(cur, prev)
+        ctx.hybrid_solve(p)
+        r, rp = ctx.residual()
+        st = ctx.iterate_to_tolerance(1, p, 0.5 * rp, 500)
+        outs.append((ctx.get_state()[0], r, rp, st.iterations, st.r_final))
+    a, b = outs
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
+
+
 def test_group_c4_size_fast():
     """C4 geometry split in 4 slabs: 50 semi-implicit APT steps, bit-identical."""
     cfg = P.config("C4")
