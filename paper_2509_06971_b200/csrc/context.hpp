@@ -57,8 +57,12 @@ struct petto_ctx {
     petto_b200::DeviceStatus* status = nullptr;  // device
     petto_b200::DeviceStatus* status_h = nullptr; // pinned host mirror
 
-    // TMA descriptors for the fused 3D kernel
-    CUtensorMap tU[3], tP[3], tE, tM;
+    // fused 3D kernel: per-cell modulus (recomputed after a property change) and
+    // TMA descriptors (outputs: the three state buffers and the residual scratch)
+    double* ecell = nullptr;
+    bool ecell_valid = false;
+    double ecell_scale = 0.0;
+    CUtensorMap tU[3], tP[3], tC, tM, tO2[4], tO1[4];
     bool tmaps = false;
 
     // design subsystem

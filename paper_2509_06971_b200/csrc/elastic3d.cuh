@@ -10,114 +10,85 @@
 //   * the unit-cell stiffness is applied in the Walsh-Hadamard corner-parity
 //     basis, where it has 45 structural nonzeros (stiffness.hpp); the forward and
 //     inverse transforms factor into x/y/z butterflies;
+//   * the cell modulus E_cell (the corner tree sum times the operator scale,
+//     state_solver.hpp:336-343) is a per-cell field computed once per property
+//     change (k_cell_modulus), so a cell costs one load instead of eight;
 //   * CTA = 8 warps: lane l <-> x = i0 + l (32 nodes), warp w <-> row j0-1+w
 //     (warp 0 is the y-halo row of cells whose top corners feed row j0);
-//   * each CTA streams along z (the outermost axis): per cell plane it keeps the
-//     previous plane's y/x-butterflies (12+1 doubles) and the top-face
-//     contributions (12 doubles) in registers, alternating two register sets so
-//     the stream needs no copies;
+//   * each CTA streams along z (the outermost axis), ZP node planes per task: per
+//     cell plane it keeps the previous plane's y/x-butterflies (12 doubles) and
+//     the top-face contributions (12 doubles) in registers;
 //   * node planes arrive by TMA (cp.async.bulk.tensor, zero-filled outside the
-//     grid) into a 5-stage shared-memory ring guarded by mbarriers, issued 4
-//     tasks ahead by one elected thread;
+//     grid) into an S-stage shared-memory ring guarded by mbarriers, issued S-1
+//     tasks ahead by one elected thread; the updated nodes leave through a
+//     double-buffered shared tile and a TMA tensor store issued at the next
+//     barrier, so no thread waits on its global stores;
 //   * x-neighbour contributions travel by warp shuffle, y-neighbour ones through
-//     a double-buffered shared tile, and the previous x-tile's last column through
-//     a small shared "x-halo" array -- a CTA walks the x-tiles of its
-//     (strip, z-chunk) item sequentially, so no cell is computed twice in x;
+//     a double-buffered shared tile (one CTA barrier per task, i.e. per ZP
+//     planes), and the previous x-tile's last column through a small shared
+//     "x-halo" array -- a CTA walks the x-tiles of its (strip, z-chunk) item
+//     sequentially, so no cell is computed twice in x;
 //   * work item = (y-strip, z-chunk); item b -> CTA b with strips fastest, so the
 //     CTAs sharing a strip boundary stream the same planes at the same time and
 //     the halo rows are served from L2.
-// Algorithmic HBM bytes per node-update: u_n 24 + u_{n-1} 24 + E 8 + u_{n+1} 24
-// (+1 mask byte); PT drops u_{n-1}.
+// Algorithmic HBM bytes per node-update: u_n 24 + u_{n-1} 24 + E_cell 8 +
+// u_{n+1} 24 (+1 mask byte); PT drops u_{n-1}.
 #pragma once
-
-#include <type_traits>
 
 #include "common.cuh"
 
 namespace petto_b200 {
 namespace e3 {
 
-// Build-time knobs (A/B variants: -DE3_W=11 -DE3_S=4 -DE3_TOP_SMEM=1 ...).
+// Build-time knobs (A/B variants: -DE3_W=7 -DE3_S=4 ...).
 #ifndef E3_W
 #define E3_W 7
 #endif
 #ifndef E3_S
-#define E3_S 5
+#define E3_S 4
 #endif
-#ifndef E3_TOP_SMEM
-#define E3_TOP_SMEM 0
-#endif
-#ifndef E3_DESYNC
-#define E3_DESYNC 0
-#endif
-#ifndef E3_CONST_KH
-#define E3_CONST_KH 0
+#ifndef E3_EXPERIMENT
+#define E3_EXPERIMENT 0  // 1: no TMA traffic (compute only), 2: no cell math (traffic only)
 #endif
 constexpr int W = E3_W;        // owned node rows per tile
 constexpr int NWARP = W + 1;   // + y-halo warp
 constexpr int NTHREADS = NWARP * 32;
-constexpr int BOXX = 34;       // TMA box width (33 columns used; 16-byte multiple)
+constexpr int ZP = 2;          // node planes per task
+constexpr int BOXX = 34;       // TMA box width of U (33 columns used; 16-byte multiple)
 constexpr int UROWS = W + 2;   // rows j0-1 .. j0+W
-constexpr int S = E3_S;        // pipeline depth
+constexpr int S = E3_S;        // pipeline depth (tasks)
 constexpr int LMAX = 64;       // longest z chunk (x-halo buffer)
-constexpr bool TOP_SMEM = E3_TOP_SMEM != 0;  // carried top-face sums in shared memory
-// DESYNC: no CTA-wide barrier per task.  Warp w hands its row-(j+1) face shares to
-// warp w+1 through a pairwise named barrier, and each warp releases a TMA stage
-// through an "empty" mbarrier; warps drift apart by up to a task, so the FP64
-// phase of one warp overlaps the load/exchange phase of another.
-constexpr bool DESYNC = E3_DESYNC != 0;
-constexpr int YD = DESYNC ? S : 2;  // depth of the y-exchange ring (>= the drift bound)
 
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
-constexpr int OFF_U = 0;                                    // [3][UROWS][BOXX] f64
-constexpr int OFF_E = r128(3 * UROWS * BOXX * 8);           // [UROWS][BOXX] f64
-constexpr int OFF_P = OFF_E + r128(UROWS * BOXX * 8);       // [3][W][32] f64
-constexpr int OFF_M = OFF_P + r128(3 * W * 32 * 8);         // [W][32] u8
-constexpr int STAGE_BYTES = OFF_M + r128(W * 32);
-constexpr uint32_t BYTES_UE = 3 * UROWS * BOXX * 8 + UROWS * BOXX * 8;
-constexpr uint32_t BYTES_P = 3 * W * 32 * 8;
-constexpr uint32_t BYTES_M = W * 32;
+constexpr int OFF_U = 0;                                      // [3][ZP][UROWS][BOXX] f64
+constexpr int OFF_C = r128(3 * ZP * UROWS * BOXX * 8);        // [ZP][NWARP][32] f64 cell modulus
+constexpr int OFF_P = OFF_C + r128(ZP * NWARP * 32 * 8);      // [3][ZP][W][32] f64
+constexpr int OFF_M = OFF_P + r128(3 * ZP * W * 32 * 8);      // [ZP][W][32] u8
+constexpr int STAGE_BYTES = OFF_M + r128(ZP * W * 32);
+constexpr uint32_t BYTES_U = 3 * ZP * UROWS * BOXX * 8;
+constexpr uint32_t BYTES_C = ZP * NWARP * 32 * 8;
+constexpr uint32_t BYTES_P = 3 * ZP * W * 32 * 8;
+constexpr uint32_t BYTES_M = ZP * W * 32;
+constexpr int USTRIDE = ZP * UROWS * BOXX;  // component stride of the U tile
+constexpr int PSTRIDE = ZP * W * 32;        // component stride of the P tile
+constexpr int YS = ZP * 6 * 32;             // one warp's y shares of one task
+constexpr int OUT_ELEMS = 3 * ZP * W * 32;  // one output tile [3][ZP][W][32] (tail: [3][1][W][32])
 
-constexpr int OFF_Y = S * STAGE_BYTES;                      // [YD][NWARP][6][32] f64
-constexpr int OFF_X = OFF_Y + YD * NWARP * 6 * 32 * 8;      // [2][LMAX][NWARP][3] f64
-constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] full, [S] empty, [W][S] y-ready
-constexpr int OFF_RED = OFF_BAR + (2 * S + W * S) * 8;      // [NWARP] f64
+constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][ZP][6][32] f64
+constexpr int OFF_X = OFF_Y + 2 * NWARP * YS * 8;           // [2][LMAX][NWARP][3] f64
+constexpr int OFF_O = OFF_X + 2 * LMAX * NWARP * 3 * 8;     // [2][OUT_ELEMS] f64
+constexpr int OFF_BAR = OFF_O + 2 * OUT_ELEMS * 8;          // [S] full
+constexpr int OFF_RED = OFF_BAR + S * 8;                    // [NWARP] f64
 constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
-constexpr int OFF_TOP = OFF_CUR + 128;                      // [12][NTHREADS] f64 (TOP_SMEM)
-constexpr int SMEM_BYTES = OFF_TOP + (TOP_SMEM ? 12 * NTHREADS * 8 : 0);
-
-// Carried top-face contributions of the previous cell plane: 12 doubles per
-// thread, in registers or in the thread's own shared-memory column.
-struct TopRegs {
-    double v[4][3];
-    __device__ __forceinline__ double& at(int q, int c) { return v[q][c]; }
-};
-struct TopSmem {
-    double* p;  // this thread's column
-    __device__ __forceinline__ double& at(int q, int c) { return p[(q * 3 + c) * NTHREADS]; }
-};
-using Top = typename std::conditional<TOP_SMEM, TopSmem, TopRegs>::type;
-__device__ __forceinline__ void bind_top(TopRegs&, unsigned char*) {}
-__device__ __forceinline__ void bind_top(TopSmem& t, unsigned char* smem) {
-    t.p = reinterpret_cast<double*>(smem + OFF_TOP) + threadIdx.x;
-}
-
-// Modal stiffness operands: from the kernel parameters (default) or from a
-// __constant__ bank refreshed on the launching stream before each launch.
-__constant__ double c_kh[48];
-#if E3_CONST_KH
-#define KH c_kh
-#else
-#define KH P.kh
-#endif
+constexpr int SMEM_BYTES = OFF_CUR + 128;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 struct Params {
     Geo g;
     double kh[45];     // modal stiffness (stiffness.hpp pattern order)
-    double e_scale;    // (sum of 8 corner E) -> E_cell: cm * 2(1+nu_op) / 8
     double inv_base;   // 1 / (hx hy hz)
-    double dt, a, b, inv;
-    double* next;      // output field (may alias the previous iterate)
+    // update coefficients: APT u' = c1 u - c2 u_prev + c3 r; PT u' = u + dt r
+    double c1, c2, c3, dt;
     const double* aux; // pinned values / loads (3 x Ns)
     double* partials;  // per-CTA sum of r^2 over unconstrained entries (nullable)
     DeviceStatus* status;
@@ -127,21 +98,33 @@ struct Params {
     int chunk;         // owned planes per z chunk (<= LMAX)
     int nitems;        // nstrips * chunks
 };
+#define KH P.kh
+
+// The tensor maps of one launch (kernel parameters, 64-byte aligned).
+struct Maps {
+    CUtensorMap u;     // state u_n: box [3][ZP][UROWS][BOXX]
+    CUtensorMap c;     // cell modulus: box [ZP][NWARP][32]
+    CUtensorMap p;     // previous iterate: box [3][ZP][W][32]
+    CUtensorMap m;     // node mask: box [ZP][W][32]
+    CUtensorMap o2;    // output: box [3][ZP][W][32]
+    CUtensorMap o1;    // output, one plane: box [3][1][W][32]
+};
 
 // Producer cursor over the CTA's task sequence: items (b, b+grid, ...), x tiles,
-// tasks kc = ka-2 (prologue), ka-1 (first cell plane), ka .. kb-1 (owned planes).
+// tasks kk = 0 (prologue: node planes ka-1, ka) and kk >= 1 (owned planes
+// kc = ka + ZP (kk-1) ..., loading node planes kc+1 .. kc+ZP).
 struct Cursor {
-    int item, t, kk, s, ka, len;
+    int item, t, kk, s, ka, ntask;
     bool valid;
     __device__ void set(const Params& P) {
         valid = item < P.nitems;
         if (!valid) return;
         s = item % P.nstrips;
         ka = P.g.kb + (item / P.nstrips) * P.chunk;
-        len = min(P.chunk, P.g.ke - ka);
+        ntask = 1 + (min(P.chunk, P.g.ke - ka) + ZP - 1) / ZP;
     }
     __device__ void next(const Params& P) {
-        if (++kk == len + 2) {
+        if (++kk == ntask) {
             kk = 0;
             if (++t == P.ntx) {
                 t = 0;
@@ -154,30 +137,35 @@ struct Cursor {
 
 template <int FORM>
 __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned char* smem, uint64_t* bars,
-                                      int stage, const CUtensorMap* tU, const CUtensorMap* tE,
-                                      const CUtensorMap* tP, const CUtensorMap* tM) {
+                                      int stage, const Maps& T) {
     unsigned char* st = smem + stage * STAGE_BYTES;
-    const bool own = c.kk >= 2;
+    const bool own = c.kk >= 1;
     const bool need_p = own && FORM <= 1;
-    const uint32_t bytes = BYTES_UE + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
+    const uint32_t bytes = BYTES_U + BYTES_C + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
+    if (E3_EXPERIMENT == 1) {
+        mbar_arrive(&bars[stage]);
+        return;
+    }
     mbar_expect_tx(&bars[stage], bytes);
-    const int i0 = c.t * 32, j0 = c.s * W, kc = c.ka - 2 + c.kk;
-    const int zn = kc + 1 - P.g.ks0;
-    tma_load_4d(st + OFF_U, tU, &bars[stage], i0, j0 - 1, zn, 0);
-    tma_load_3d(st + OFF_E, tE, &bars[stage], i0, j0 - 1, zn);
+    const int i0 = c.t * 32, j0 = c.s * W;
+    // first cell plane of the task; the node planes loaded are kc+1, kc+2 for an
+    // owned task and kc, kc+1 (= ka-1, ka) for the prologue
+    const int kc = own ? c.ka + ZP * (c.kk - 1) : c.ka - 1;
+    tma_load_4d(st + OFF_U, &T.u, &bars[stage], i0, j0 - 1, kc + (own ? 1 : 0) - P.g.ks0, 0);
+    tma_load_3d(st + OFF_C, &T.c, &bars[stage], i0, j0 - 1, kc - P.g.ks0);
     if (own) {
-        tma_load_3d(st + OFF_M, tM, &bars[stage], i0, j0, kc - P.g.ks0);
-        if (need_p) tma_load_4d(st + OFF_P, tP, &bars[stage], i0, j0, kc - P.g.ks0, 0);
+        tma_load_3d(st + OFF_M, &T.m, &bars[stage], i0, j0, kc - P.g.ks0);
+        if (need_p) tma_load_4d(st + OFF_P, &T.p, &bars[stage], i0, j0, kc - P.g.ks0, 0);
     }
 }
 
 // Everything a task needs that is fixed for one x-tile of one item.
 struct Tile {
-    int i, j, t;
+    int t;
     bool upd;            // this thread owns a grid node of the tile
-    double escale;       // e_scale, or 0 where the cell (i, j) is outside the grid
-    double invv_xy;      // 1/V without the z-end factor
-    long long node0;     // lidx(i, j, 0)
+    double ninv;         // -1/V at an interior z plane
+    double ninv_end;     // -1/V at z = 0 or nz-1
+    long long node0;     // lidx(i, j, 0) (loads and pinned values)
     double* xw;          // x-halo out (lane 31) / in (lane 0)
     const double* xr;
 };
@@ -187,14 +175,17 @@ struct Pipe {
     uint64_t* bars;
     int st, q;
     uint32_t phase;
+    // output tile waiting for the next barrier: planes (0 none, 1, 2), origin, buffer
+    int pst, px, py, pz, pbuf;
+    int ob;              // buffer of the next owned task's output tile
 };
 
-// forward x/y butterflies of node plane kc+1 for cell (i, j): B[sx + 2 sy][c], E sum
-__device__ __forceinline__ void forward(const unsigned char* sb, int w, int l, double (&B)[4][3], double& E) {
-    const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
+// forward x/y butterflies of stage plane z for cell (i, j): B[sx + 2 sy][c]
+__device__ __forceinline__ void forward(const unsigned char* sb, int z, int w, int l, double (&B)[4][3]) {
+    const double* su = reinterpret_cast<const double*>(sb + OFF_U) + (z * UROWS + w) * BOXX + l;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double* r0 = su + c * UROWS * BOXX;
+        const double* r0 = su + c * USTRIDE;
         const double a = r0[0], b = r0[1], cc = r0[BOXX], d = r0[BOXX + 1];
         const double A0 = a + b, A1 = a - b, A0n = cc + d, A1n = cc - d;
         B[0][c] = A0 + A0n;
@@ -202,21 +193,33 @@ __device__ __forceinline__ void forward(const unsigned char* sb, int w, int l, d
         B[2][c] = A0 - A0n;
         B[3][c] = A1 - A1n;
     }
-    const double* e0 = reinterpret_cast<const double*>(sb + OFF_E) + w * BOXX + l;
-    E = (e0[0] + e0[1]) + (e0[BOXX] + e0[BOXX + 1]);
 }
 
-// z butterflies, modal stiffness, inverse z butterflies: bottom face (node plane
-// kc) returned in face (added to the carried top), new top carried out.
+// z butterflies, modal stiffness, inverse z butterflies of one cell with modulus
+// ec: bottom face (node plane kc) assembled with the carried top, new top carried
+// out; with EMIT the inverse y butterflies of the face: row j's sums in Yj, row
+// j+1's shares to sYw.  The modulus multiplies the modal forces inside the face
+// sums (fused multiply-adds) instead of the 21 modal inputs.
 template <bool EMIT>
-__device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], double Ec, const double (&Bn)[4][3],
-                                     double En, double escale, Top& top, double (&Yj)[2][3], double* sYw) {
-    const double ec = (Ec + En) * escale;
-    // modal coefficients C[s] = E_cell * (z butterfly), s = sx + 2 sy + 4 sz; the
-    // modal stiffness decouples into blocks {1,2,4}, {3,5,6}, {7}, evaluated and
-    // consumed one after the other to keep few values live.
-    auto Cp = [&](int q, int c) { return (Bc[q][c] + Bn[q][c]) * ec; };  // sz = 0
-    auto Cm = [&](int q, int c) { return (Bc[q][c] - Bn[q][c]) * ec; };  // sz = 1
+__device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], const double (&Bn)[4][3], double ec,
+                                     double (&top)[4][3], double (&Yj)[2][3], double* sYw) {
+    if (E3_EXPERIMENT == 2) {
+        if (EMIT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                Yj[0][c] = Bc[0][c] + Bn[1][c];
+                Yj[1][c] = Bc[2][c] + Bn[3][c] + ec;
+                sYw[c * 32] = Bc[1][c];
+                sYw[(3 + c) * 32] = Bn[2][c];
+            }
+        }
+        return;
+    }
+    // modal coefficients C[s] (z butterflies), s = sx + 2 sy + 4 sz; the modal
+    // stiffness decouples into blocks {1,2,4}, {3,5,6}, {7}, evaluated and consumed
+    // one after the other to keep few values live.
+    auto Cp = [&](int q, int c) { return Bc[q][c] + Bn[q][c]; };  // sz = 0
+    auto Cm = [&](int q, int c) { return Bc[q][c] - Bn[q][c]; };  // sz = 1
     // block A: linear modes 1 (x), 2 (y), 4 (z)
     const double c10 = Cp(1, 0), c11 = Cp(1, 1), c12 = Cp(1, 2);
     const double c20 = Cp(2, 0), c21 = Cp(2, 1), c22 = Cp(2, 2);
@@ -230,14 +233,17 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     const double F40 = KH[14] * c12 + KH[15] * c40;
     const double F41 = KH[16] * c22 + KH[17] * c41;
     const double F42 = KH[18] * c10 + KH[19] * c21 + KH[20] * c42;
-    // pair (0, 4): mode 0 (rigid translation) carries no force
+    // pair (0, 4): mode 0 (rigid translation) carries no force; the carried top
+    // of this pair is stored with the opposite sign
     double f0[3];
-    f0[0] = top.at(0, 0) + F40;
-    f0[1] = top.at(0, 1) + F41;
-    f0[2] = top.at(0, 2) + F42;
-    top.at(0, 0) = -F40;
-    top.at(0, 1) = -F41;
-    top.at(0, 2) = -F42;
+    {
+        const double F4[3] = {F40, F41, F42};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            f0[c] = fma(ec, F4[c], -top[0][c]);
+            top[0][c] = ec * F4[c];
+        }
+    }
     // block B: bilinear modes 3 (xy), 5 (xz), 6 (yz)
     const double c30 = Cp(3, 0), c31 = Cp(3, 1), c32 = Cp(3, 2);
     const double c50 = Cm(1, 0), c51 = Cm(1, 1), c52 = Cm(1, 2);
@@ -252,36 +258,32 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     const double F61 = KH[38] * c50 + KH[39] * c61;
     const double F62 = KH[40] * c30 + KH[41] * c62;
     // pairs (1, 5) and (2, 6)
-    double f1[3];
-    f1[0] = top.at(1, 0) + (F10 + F50);
-    f1[1] = top.at(1, 1) + (F11 + F51);
-    f1[2] = top.at(1, 2) + (F12 + F52);
-    top.at(1, 0) = F10 - F50;
-    top.at(1, 1) = F11 - F51;
-    top.at(1, 2) = F12 - F52;
-    const double f20 = top.at(2, 0) + (F20 + F60);
-    const double f21 = top.at(2, 1) + (F21 + F61);
-    const double f22 = top.at(2, 2) + (F22 + F62);
-    top.at(2, 0) = F20 - F60;
-    top.at(2, 1) = F21 - F61;
-    top.at(2, 2) = F22 - F62;
-    // inverse y butterflies of the sx = 0 face modes: row j keeps the sum, row j+1
-    // (warp w+1) gets the difference through shared memory
+    double f1[3], f2[3];
+    {
+        const double F1[3] = {F10, F11, F12}, F5[3] = {F50, F51, F52};
+        const double F2[3] = {F20, F21, F22}, F6[3] = {F60, F61, F62};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            f1[c] = fma(ec, F1[c] + F5[c], top[1][c]);
+            top[1][c] = ec * (F1[c] - F5[c]);
+            f2[c] = fma(ec, F2[c] + F6[c], top[2][c]);
+            top[2][c] = ec * (F2[c] - F6[c]);
+        }
+    }
     if (EMIT) {
-        Yj[0][0] = f0[0] + f20;
-        Yj[0][1] = f0[1] + f21;
-        Yj[0][2] = f0[2] + f22;
-        sYw[0 * 32] = f0[0] - f20;
-        sYw[1 * 32] = f0[1] - f21;
-        sYw[2 * 32] = f0[2] - f22;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            Yj[0][c] = f0[c] + f2[c];
+            sYw[c * 32] = f0[c] - f2[c];
+        }
     }
     // block C: trilinear mode 7, pair (3, 7), then the sx = 1 face modes
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const double F7 = KH[42 + c] * Cm(3, c);
         const double F3 = c == 0 ? F30 : (c == 1 ? F31 : F32);
-        const double f3 = top.at(3, c) + (F3 + F7);
-        top.at(3, c) = F3 - F7;
+        const double f3 = fma(ec, F3 + F7, top[3][c]);
+        top[3][c] = ec * (F3 - F7);
         if (EMIT) {
             Yj[1][c] = f1[c] + f3;
             sYw[(3 + c) * 32] = f1[c] - f3;
@@ -289,49 +291,28 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     }
 }
 
-// Mid-task hand-off (after the y shares are written).  Synchronous mode: one CTA
-// barrier, then the producer refills the stage of the previous task.
+// Barrier after the y shares are written.  Then the producer refills the stage of
+// the previous task (every warp is past its last read of it) and issues the TMA
+// store of the output tile finished before the barrier; before the barrier it
+// waits until the store issued at the previous barrier has read its buffer (the
+// buffer the coming node phase overwrites).
 template <int FORM>
-__device__ __forceinline__ void end_task(const Params& P, Pipe& pp, Cursor* pc, const CUtensorMap* tU,
-                                         const CUtensorMap* tE, const CUtensorMap* tP, const CUtensorMap* tM) {
-    if (DESYNC) return;
+__device__ __forceinline__ void end_task(const Params& P, Pipe& pp, Cursor* pc, const Maps& T) {
+    fence_proxy_async();  // this thread's output-tile writes -> async proxy
+    if (threadIdx.x == 0) bulk_wait_read();
     __syncthreads();
-    if (threadIdx.x == 0 && pc->valid) {
-        issue<FORM>(P, *pc, pp.smem, pp.bars, pp.st == 0 ? S - 1 : pp.st - 1, tU, tE, tP, tM);
-        pc->next(P);
+    if (threadIdx.x == 0) {
+        if (pc->valid) {
+            issue<FORM>(P, *pc, pp.smem, pp.bars, pp.st == 0 ? S - 1 : pp.st - 1, T);
+            pc->next(P);
+        }
+        if (pp.pst && E3_EXPERIMENT != 1) {
+            const double* src = reinterpret_cast<const double*>(pp.smem + OFF_O) + pp.pbuf * OUT_ELEMS;
+            tma_store_4d(pp.pst == 2 ? &T.o2 : &T.o1, src, pp.px, pp.py, pp.pz, 0);
+            bulk_commit();
+        }
     }
-}
-
-// End of a task (after the warp's last read of the stage).  Desync mode: the warp
-// releases the stage; thread 0 refills the stage of the previous task once every
-// warp has released it.
-template <int FORM>
-__device__ __forceinline__ void release(const Params& P, Pipe& pp, Cursor* pc, const CUtensorMap* tU,
-                                        const CUtensorMap* tE, const CUtensorMap* tP, const CUtensorMap* tM) {
-    if (!DESYNC) return;
-    __syncwarp();
-    uint64_t* empty = pp.bars + S;
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[pp.st]);
-    if (threadIdx.x == 0 && pc->valid) {
-        const int prev = pp.st == 0 ? S - 1 : pp.st - 1;
-        if (pp.q >= 1) mbar_wait(&empty[prev], pp.st == 0 ? pp.phase ^ 1u : pp.phase);
-        issue<FORM>(P, *pc, pp.smem, pp.bars, prev, tU, tE, tP, tM);
-        pc->next(P);
-    }
-}
-
-// The y-ready barriers complete one phase per task, so tasks without a y exchange
-// (prologue, first cell plane) still hand off to keep the phases aligned with the
-// task counter.
-__device__ __forceinline__ void y_handoff(Pipe& pp) {
-    if (!DESYNC) return;
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint64_t* yready = pp.bars + 2 * S;
-    if (w < W) {
-        __syncwarp();
-        if (l == 0) mbar_arrive(&yready[w * S + pp.st]);
-    }
-    if (w > 0) mbar_wait(&yready[(w - 1) * S + pp.st], pp.phase);
+    pp.pst = 0;
 }
 
 __device__ __forceinline__ void advance(Pipe& pp) {
@@ -342,48 +323,22 @@ __device__ __forceinline__ void advance(Pipe& pp) {
     }
 }
 
-// One owned node plane kc: forward of plane kc+1 into Bn, cell plane kc, face
-// assembly, node update of (i, j, kc).
+// Node (i, j, kc): edge sums with warp w-1's shares, inverse x butterflies (x-halo
+// for lane 0), then the residual, the update and the write into the output tile
+// (component stride ocs).  u_n arrives in u.
 template <int FORM>
-__device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, const Tile& T, int kc, int zi,
-                                         const double (&Bc)[4][3], double Ec, double (&Bn)[4][3], double& En,
-                                         Top& top, double (&ucar)[3], double& rsq, unsigned& bad,
-                                         double* sY, const CUtensorMap* tU, const CUtensorMap* tE,
-                                         const CUtensorMap* tP, const CUtensorMap* tM) {
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+__device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int zi, const double (&Yj)[2][3],
+                                     const double* below, const double (&u)[3], const double* sp,
+                                     unsigned char mk, double* out, int ocs, double& rsq, unsigned& bad) {
+    const int l = threadIdx.x & 31;
     const Geo& g = P.g;
-    mbar_wait(&pp.bars[pp.st], pp.phase);
-    const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
-    forward(sb, w, l, Bn, En);
-    // cell plane kc with the inverse y butterflies: row j's sums in Yj, row j+1's
-    // shares to warp w+1 through shared memory
-    double* sYw = sY + (DESYNC ? pp.st : (pp.q & 1)) * (NWARP * 6 * 32);
-    double Yj[2][3];
-    cell<true>(P, Bc, Ec, Bn, En, kc <= g.nz - 2 ? T.escale : 0.0, top, Yj, sYw + w * 6 * 32 + l);
-    uint64_t* yready = pp.bars + 2 * S;  // [W][S]: warp w's shares of task q ready
-    if (DESYNC && w < W) {
-        __syncwarp();
-        if (l == 0) mbar_arrive(&yready[w * S + pp.st]);
-    }
-    end_task<FORM>(P, pp, pc, tU, tE, tP, tM);
-    // edge sums (w >= 1), inverse x butterflies, node assembly
     double Xi[3], Xn[3];
-    if (w > 0) {  // warp-uniform
-        if (DESYNC) mbar_wait(&yready[(w - 1) * S + pp.st], pp.phase);
-        const double* below = sYw + (w - 1) * 6 * 32 + l;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double e0v = Yj[0][c] + below[c * 32];
-            const double e1v = Yj[1][c] + below[(3 + c) * 32];
-            Xi[c] = e0v + e1v;
-            Xn[c] = e0v - e1v;
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            Xi[c] = Yj[0][c] + Yj[1][c];
-            Xn[c] = Yj[0][c] - Yj[1][c];
-        }
+    for (int c = 0; c < 3; ++c) {
+        const double e0v = Yj[0][c] + below[c * 32];
+        const double e1v = Yj[1][c] + below[(3 + c) * 32];
+        Xi[c] = e0v + e1v;
+        Xn[c] = e0v - e1v;
     }
     double acc[3];
     const double* xr = T.xr + zi * (NWARP * 3);
@@ -397,101 +352,133 @@ __device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, 
 #pragma unroll
         for (int c = 0; c < 3; ++c) xw[c] = Xn[c];
     }
-    if (T.upd) {
-        const unsigned char mk = (sb + OFF_M)[(w - 1) * 32 + l];
-        const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (w - 1) * 32 + l;
-        const double invv = (kc == 0 || kc == g.nz - 1) ? 2.0 * T.invv_xy : T.invv_xy;
-        const long long node = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
-        auto update = [&](int c, double r) {
-            if (FORM == 0) {
-                const double cu = ucar[c], pv = sp[c * W * 32];
-                return 2.0 * cu - pv + P.a * r - P.b * (cu - pv);
-            } else if (FORM == 1) {
-                const double cu = ucar[c], pv = sp[c * W * 32];
-                return (2.0 * cu - pv + P.b * cu + P.a * r) * P.inv;
-            } else if (FORM == 2) {
-                return ucar[c] + P.dt * r;
-            }
-            return r;
-        };
-        double nv[3];
-        if (!mk) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double r = -acc[c] * invv;
-                nv[c] = update(c, r);
-                rsq += r * r;
-            }
-        } else {  // rare: pinned components and/or a load on this node
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const bool pinned = (mk >> c) & 1;
-                const double f = ((mk & 8) && !pinned) ? P.aux[c * g.Ns + node] : 0.0;
-                const double r = -acc[c] * invv - f;
-                if (pinned) {
-                    nv[c] = FORM == 3 ? 0.0 : P.aux[c * g.Ns + node];
-                } else {
-                    rsq += r * r;
-                    nv[c] = update(c, r);
-                }
-            }
-        }
-        // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
-        unsigned ex = 0;
+    if (!T.upd) return;
+    const double ninv = (kc == 0 || kc == g.nz - 1) ? T.ninv_end : T.ninv;  // warp-uniform select
+    auto update = [&](int c, double r) {
+        if (FORM <= 1) return fma(P.c1, u[c], fma(-P.c2, sp[c * PSTRIDE], P.c3 * r));
+        if (FORM == 2) return fma(P.dt, r, u[c]);
+        return r;
+    };
+    double nv[3];
+    if (!mk) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
-            P.next[c * g.Ns + node] = nv[c];
+            const double r = acc[c] * ninv;
+            nv[c] = update(c, r);
+            rsq = fma(r, r, rsq);
         }
-        bad |= ex;
-    }
-    // own node of plane kc+1 feeds the next task's update (this stage is only
-    // recycled after the next task's barrier)
-    const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
+    } else {  // rare: pinned components and/or a load on this node
+        const long long node = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
-    release<FORM>(P, pp, pc, tU, tE, tP, tM);
+        for (int c = 0; c < 3; ++c) {
+            const bool pinned = (mk >> c) & 1;
+            const double f = ((mk & 8) && !pinned) ? P.aux[c * g.Ns + node] : 0.0;
+            const double r = acc[c] * ninv - f;
+            if (pinned) {
+                nv[c] = FORM == 3 ? 0.0 : P.aux[c * g.Ns + node];
+            } else {
+                rsq = fma(r, r, rsq);
+                nv[c] = update(c, r);
+            }
+        }
+    }
+    // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
+    unsigned ex = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
+        out[c * ocs] = nv[c];
+    }
+    bad |= ex;
+}
+
+// Owned node planes kc (and kc+1 when two): forward of node planes kc+1, kc+2,
+// cell planes kc, kc+1, one barrier, then the node planes into the output tile.
+// On entry Bc holds the butterflies of node plane kc and ucar its u_n; on exit
+// both describe kc+2.
+template <int FORM>
+__device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, const Maps& M, const Tile& T,
+                                         int s, int kc, int zi, bool two, double (&Bc)[4][3], double (&top)[4][3],
+                                         double (&ucar)[3], double& rsq, unsigned& bad, double* sY) {
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const Geo& g = P.g;
+    mbar_wait(&pp.bars[pp.st], pp.phase);
+    const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
+    double* sYt = sY + (pp.q & 1) * (NWARP * YS);
+    double* sYw = sYt + w * YS + l;
+    const double* sc = reinterpret_cast<const double*>(sb + OFF_C) + w * 32 + l;
+    double B1[4][3], Y0[2][3], Y1[2][3];
+    forward(sb, 0, w, l, B1);
+    cell<true>(P, Bc, B1, sc[0], top, Y0, sYw);
+    if (two) {  // warp-uniform
+        forward(sb, 1, w, l, Bc);
+        cell<true>(P, B1, Bc, sc[NWARP * 32], top, Y1, sYw + 6 * 32);
+    }
+    end_task<FORM>(P, pp, pc, M);
+    const int ob = pp.ob;
+    pp.ob ^= 1;
+    pp.pst = two ? 2 : 1;
+    pp.px = T.t * 32;
+    pp.py = s * W;
+    pp.pz = kc - g.ks0;
+    pp.pbuf = ob;
+    if (w > 0) {  // warp-uniform: warp 0 (the y-halo row) only emits shares
+        const double* below = sYt + (w - 1) * YS + l;
+        const unsigned char* mk = sb + OFF_M + (w - 1) * 32 + l;
+        const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (w - 1) * 32 + l;
+        const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;  // node plane kc+1
+        double* out = reinterpret_cast<double*>(pp.smem + OFF_O) + ob * OUT_ELEMS + (w - 1) * 32 + l;
+        const int ocs = two ? ZP * W * 32 : W * 32;
+        node<FORM>(P, T, kc, zi, Y0, below, ucar, sp, mk[0], out, ocs, rsq, bad);
+        if (two) {
+            double u1[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
+            node<FORM>(P, T, kc + 1, zi + 1, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32], out + W * 32, ocs,
+                       rsq, bad);
+        }
+        // node plane kc+2 feeds the next task (this stage is only recycled after
+        // the next task's barrier)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE + UROWS * BOXX];
+    }
     advance(pp);
 }
 
 template <int FORM>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap tU,
-                     const __grid_constant__ CUtensorMap tE, const __grid_constant__ CUtensorMap tP,
-                     const __grid_constant__ CUtensorMap tM) {
+    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
     if (skip_step(P.status, P.step, P.nsteps)) return;
-    Pipe pp{smem, reinterpret_cast<uint64_t*>(smem + OFF_BAR), 0, 0, 0u};
+    Pipe pp{smem, reinterpret_cast<uint64_t*>(smem + OFF_BAR), 0, 0, 0u, 0, 0, 0, 0, 0, 0};
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
     Cursor* pc = reinterpret_cast<Cursor*>(smem + OFF_CUR);
+    if (E3_EXPERIMENT == 1)  // compute-only runs read a zeroed ring
+        for (int b = threadIdx.x; b < S * STAGE_BYTES / 4; b += NTHREADS) reinterpret_cast<uint32_t*>(smem)[b] = 0u;
     if (threadIdx.x == 0) {
-        prefetch_tmap(&tU);
-        prefetch_tmap(&tE);
-        prefetch_tmap(&tP);
-        prefetch_tmap(&tM);
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&pp.bars[s], 1);          // full: the producer's expect_tx + TMA bytes
-            mbar_init(&pp.bars[S + s], NWARP);  // empty: one arrival per warp
-        }
-        for (int b = 0; b < W * S; ++b) mbar_init(&pp.bars[2 * S + b], 1);  // y-ready: producer lane 0
+        prefetch_tmap(&M.u);
+        prefetch_tmap(&M.c);
+        prefetch_tmap(&M.p);
+        prefetch_tmap(&M.m);
+        prefetch_tmap(&M.o2);
+        prefetch_tmap(&M.o1);
+        for (int s = 0; s < S; ++s) mbar_init(&pp.bars[s], 1);  // the producer's expect_tx + TMA bytes
         fence_mbar_init();
         pc->item = blockIdx.x;
         pc->t = 0;
         pc->kk = 0;
         pc->set(P);
         for (int s = 0; s < S - 1 && pc->valid; ++s) {
-            issue<FORM>(P, *pc, smem, pp.bars, s, &tU, &tE, &tP, &tM);
+            issue<FORM>(P, *pc, smem, pp.bars, s, M);
             pc->next(P);
         }
     }
     __syncthreads();
 
-    double BA[4][3], BB[4][3], EA = 0.0, EB = 0.0, ucar[3] = {0.0, 0.0, 0.0};
-    Top top;
-    bind_top(top, smem);
+    double Bc[4][3], top[4][3], ucar[3] = {0.0, 0.0, 0.0};
     double rsq = 0.0;
     unsigned bad = 0;
     for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
@@ -501,55 +488,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int t = 0; t < P.ntx; ++t) {
             Tile T;
             T.t = t;
-            T.i = t * 32 + l;
-            T.j = s * W - 1 + w;
-            T.upd = w >= 1 && T.i < g.nx && T.j < g.ny;
-            const bool cxy = T.i <= g.nx - 2 && T.j >= 0 && T.j <= g.ny - 2;
-            T.escale = cxy ? P.e_scale : 0.0;
-            const int ends = (T.i == 0 || T.i == g.nx - 1) + (T.j == 0 || T.j == g.ny - 1);
-            T.invv_xy = P.inv_base * (double)(1 << ends);
-            T.node0 = (long long)max(T.j, 0) * g.px + T.i;
+            const int i = t * 32 + l, j = s * W - 1 + w;
+            T.upd = w >= 1 && i < g.nx && j < g.ny;
+            const int ends = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
+            T.ninv = -P.inv_base * (double)(1 << ends);
+            T.ninv_end = 2.0 * T.ninv;
+            T.node0 = (long long)max(j, 0) * g.px + i;
             T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + w * 3;
             T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + w * 3;
 
-            // prologue: butterflies of node plane ka-1
-            mbar_wait(&pp.bars[pp.st], pp.phase);
-            forward(pp.smem + pp.st * STAGE_BYTES, w, l, BA, EA);
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) top.at(q4, c) = 0.0;
-            end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
-            y_handoff(pp);
-            release<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
-            advance(pp);
-            // first cell plane ka-1: its top face feeds node plane ka
+            // prologue: butterflies of node planes ka-1 and ka, cell plane ka-1
+            // (its top face feeds node plane ka)
             {
                 mbar_wait(&pp.bars[pp.st], pp.phase);
                 const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
-                forward(sb, w, l, BB, EB);
-                double Yj[2][3];
-                cell<false>(P, BA, EA, BB, EB, ka - 1 >= 0 ? T.escale : 0.0, top, Yj, nullptr);
-                end_task<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
-                const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;
+                double B0[4][3], Yd[2][3];
+                forward(sb, 0, w, l, B0);
+                forward(sb, 1, w, l, Bc);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) ucar[c] = su[c * UROWS * BOXX];
-                y_handoff(pp);
-                release<FORM>(P, pp, pc, &tU, &tE, &tP, &tM);
+                for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+                const double ec = reinterpret_cast<const double*>(sb + OFF_C)[w * 32 + l];
+                cell<false>(P, B0, Bc, ec, top, Yd, nullptr);
+                const double* su = reinterpret_cast<const double*>(sb + OFF_U) + (UROWS + w) * BOXX + l;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE];
+                end_task<FORM>(P, pp, pc, M);
                 advance(pp);
             }
-            // owned planes, two per iteration with alternating register roles
-            int kc = ka;
-            for (; kc + 1 < kb; kc += 2) {
-                own_task<FORM>(P, pp, pc, T, kc, kc - ka, BB, EB, BA, EA, top, ucar, rsq, bad, sY, &tU, &tE, &tP,
-                               &tM);
-                own_task<FORM>(P, pp, pc, T, kc + 1, kc + 1 - ka, BA, EA, BB, EB, top, ucar, rsq, bad, sY, &tU,
-                               &tE, &tP, &tM);
-            }
-            if (kc < kb)
-                own_task<FORM>(P, pp, pc, T, kc, kc - ka, BB, EB, BA, EA, top, ucar, rsq, bad, sY, &tU, &tE, &tP,
-                               &tM);
+            for (int kc = ka; kc < kb; kc += ZP)
+                own_task<FORM>(P, pp, pc, M, T, s, kc, kc - ka, kc + 1 < kb, Bc, top, ucar, rsq, bad, sY);
         }
+    }
+    // the last output tile
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (pp.pst && E3_EXPERIMENT != 1) {
+            const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pp.pbuf * OUT_ELEMS;
+            tma_store_4d(pp.pst == 2 ? &M.o2 : &M.o1, src, pp.px, pp.py, pp.pz, 0);
+            bulk_commit();
+        }
+        bulk_wait_all();
     }
 
     // CTA reduction of r^2 (fixed order) and the non-finite flag
@@ -564,7 +545,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int k = 0; k < NWARP; ++k) sum += red[k];
         if (P.partials) P.partials[blockIdx.x] = sum;
     }
-    if (bad && l == 0) mark_bad(P.status, P.step);
+    if (E3_EXPERIMENT == 0 && bad && l == 0) mark_bad(P.status, P.step);
+}
+
+// Cell modulus of every stored cell (i, j, k), k = ks0 + kl: the operator scale
+// times the corner sum (the association of the fused kernel's former in-tile
+// sum), 0 where the cell lies outside the grid or its top plane is not stored.
+__global__ void k_cell_modulus(Geo g, const double* __restrict__ prop, double scale, double* __restrict__ ec) {
+    const long long n = (long long)g.px * g.ny * g.nzs;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(t % g.px);
+        const int j = (int)((t / g.px) % g.ny);
+        const int kl = (int)(t / ((long long)g.px * g.ny));
+        const int k = g.ks0 + kl;
+        double v = 0.0;
+        if (i <= g.nx - 2 && j <= g.ny - 2 && k <= g.nz - 2 && kl + 1 < g.nzs) {
+            const double* e0 = prop + t;
+            const double* e1 = e0 + (long long)g.px * g.ny;
+            const double a = (e0[0] + e0[1]) + (e0[g.px] + e0[g.px + 1]);
+            const double b = (e1[0] + e1[1]) + (e1[g.px] + e1[g.px + 1]);
+            v = (a + b) * scale;
+        }
+        ec[t] = v;
+    }
 }
 
 }  // namespace e3

@@ -113,37 +113,42 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// TMA descriptors of the fused 3D kernel.  No L2 sector promotion: the 34-column
-// U/E boxes start 256 B-aligned and would drag a second 256 B block each, and the
-// 32-byte mask rows a full 256 B block (measured: 1.6x the algorithmic reads).
+// TMA descriptors of the fused 3D kernel (and its cell-modulus field).  No L2
+// sector promotion: the 34-column U boxes start 256 B-aligned and would drag a
+// second 256 B block each, and the 32-byte mask rows a full 256 B block
+// (measured: 1.6x the algorithmic reads).
 int make_tmaps(petto_ctx* ctx) {
     const Geo& g = ctx->g;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return fail(ctx, PETTO_ERROR, "cuTensorMapEncodeTiled unavailable");
+    if (!ctx->ecell && cudaMalloc(&ctx->ecell, (size_t)g.Ns * sizeof(double)) != cudaSuccess)
+        return fail(ctx, PETTO_ERROR, "out of device memory (cell modulus)");
     const cuuint64_t d4[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs, 3};
     const cuuint64_t s4[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8, (cuuint64_t)g.Ns * 8};
-    const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, 1, 3};
-    const cuuint32_t boxP[4] = {32, e3::W, 1, 3};
+    const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, e3::ZP, 3};
+    const cuuint32_t boxP[4] = {32, e3::W, e3::ZP, 3};
+    const cuuint32_t boxO1[4] = {32, e3::W, 1, 3};
     const cuuint32_t one[4] = {1, 1, 1, 1};
-    for (int b = 0; b < 3; ++b) {
-        if (enc(&ctx->tU[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxU, one,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    auto map4 = [&](CUtensorMap* m, double* base, const cuuint32_t* box) {
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, d4, s4, box, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    for (int b = 0; b < 4; ++b) {
+        double* base = b < 3 ? ctx->st[b] : ctx->r;
+        if ((b < 3 && (!map4(&ctx->tU[b], base, boxU) || !map4(&ctx->tP[b], base, boxP))) ||
+            !map4(&ctx->tO2[b], base, boxP) || !map4(&ctx->tO1[b], base, boxO1))
             return fail(ctx, PETTO_ERROR, "tensor map (state) encode failed");
-        if (enc(&ctx->tP[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->st[b], d4, s4, boxP, one,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return fail(ctx, PETTO_ERROR, "tensor map (previous) encode failed");
     }
     const cuuint64_t d3[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs};
     const cuuint64_t s3[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8};
-    const cuuint32_t boxE[3] = {e3::BOXX, e3::UROWS, 1};
-    if (enc(&ctx->tE, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->prop, d3, s3, boxE, one,
+    const cuuint32_t boxC[3] = {32, e3::NWARP, e3::ZP};
+    if (enc(&ctx->tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->ecell, d3, s3, boxC, one,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return fail(ctx, PETTO_ERROR, "tensor map (modulus) encode failed");
+        return fail(ctx, PETTO_ERROR, "tensor map (cell modulus) encode failed");
     const cuuint64_t sm[2] = {(cuuint64_t)g.px, (cuuint64_t)g.px * g.ny};
-    const cuuint32_t boxM[3] = {32, e3::W, 1};
+    const cuuint32_t boxM[3] = {32, e3::W, e3::ZP};
     if (enc(&ctx->tM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->mask, d3, sm, boxM, one,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -287,17 +292,30 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
         const long long owned = owned_nodes(ctx);
         if (g.dim == 3 && ctx->desc.physics == 1) {
             if (!ctx->tmaps && make_tmaps(ctx)) return PETTO_ERROR;
+            const double nu = ctx->desc.poisson_ratio;
+            const double e_scale =
+                (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
+            if (!ctx->ecell_valid || ctx->ecell_scale != e_scale) {
+                e3::k_cell_modulus<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(g, ctx->prop, e_scale, ctx->ecell);
+                ctx->launches++;
+                CKL();
+                ctx->ecell_valid = true;
+                ctx->ecell_scale = e_scale;
+            }
             e3::Params P{};
             P.g = g;
             for (int i = 0; i < 45; ++i) P.kh[i] = ctx->kh[i];
-            const double nu = ctx->desc.poisson_ratio;
-            P.e_scale = (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
             P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
+            if (k.form == 0) {  // 2u - u_prev + a r - b (u - u_prev)
+                P.c1 = 2.0 - k.b;
+                P.c2 = 1.0 - k.b;
+                P.c3 = k.a;
+            } else if (k.form == 1) {  // (2u - u_prev + b u + a r) / (1 + b)
+                P.c1 = (2.0 + k.b) * k.inv;
+                P.c2 = k.inv;
+                P.c3 = k.a * k.inv;
+            }
             P.dt = k.dt;
-            P.a = k.a;
-            P.b = k.b;
-            P.inv = k.inv;
-            P.next = next;
             P.aux = ctx->aux;
             P.partials = partials;
             P.status = ctx->status;
@@ -309,22 +327,30 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             plan_3d(ctx, P.nstrips, chunks, grid);
             const int nzo = g.ke - g.kb;
             P.chunk = (nzo + chunks - 1) / chunks;
+            P.chunk += P.chunk & 1;  // even chunks: whole two-plane tasks
+            P.chunk = std::min(P.chunk, e3::LMAX);
             P.nitems = P.nstrips * ((nzo + P.chunk - 1) / P.chunk);
             grid = std::min(grid, P.nitems);
             if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
-#if E3_CONST_KH
-            // stream-ordered refresh of the constant bank the kernel reads the
-            // modal stiffness from (contexts that share a device serialise here)
-            CK(cudaMemcpyToSymbolAsync(e3::c_kh, P.kh, sizeof(double) * 45, 0, cudaMemcpyHostToDevice,
-                                       ctx->stream));
-#endif
+            int ob = -1;
+            for (int b = 0; b < 3; ++b)
+                if (next == ctx->st[b]) ob = b;
+            if (next == ctx->r) ob = 3;
+            if (ob < 0) return fail(ctx, PETTO_ERROR, "fused 3D step: output is not a context buffer");
+            e3::Maps M;
+            M.u = ctx->tU[cur];
+            M.c = ctx->tC;
+            M.p = ctx->tP[prev];
+            M.m = ctx->tM;
+            M.o2 = ctx->tO2[ob];
+            M.o1 = ctx->tO1[ob];
             timing_begin(ctx, ev);
             const int smem = e3::SMEM_BYTES;
             switch (k.form) {
-                case 0: e3::k_elastic3d_fast<0><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
-                case 1: e3::k_elastic3d_fast<1><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
-                case 2: e3::k_elastic3d_fast<2><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
-                default: e3::k_elastic3d_fast<3><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, ctx->tU[cur], ctx->tE, ctx->tP[prev], ctx->tM); break;
+                case 0: e3::k_elastic3d_fast<0><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
+                case 1: e3::k_elastic3d_fast<1><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
+                case 2: e3::k_elastic3d_fast<2><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
+                default: e3::k_elastic3d_fast<3><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
             }
             timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
             ctx->launches++;
@@ -628,6 +654,7 @@ void petto_dev_destroy(petto_ctx* ctx) {
     if (ctx->ev_pull) cudaEventDestroy(ctx->ev_pull);
     for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
     cudaFree(ctx->prop);
+    cudaFree(ctx->ecell);
     cudaFree(ctx->aux);
     cudaFree(ctx->mask);
     cudaFree(ctx->src);
@@ -763,6 +790,7 @@ int petto_dev_set_source(petto_ctx* ctx, const double* source) {
 int petto_dev_set_property(petto_ctx* ctx, const double* property) {
     CK(cudaSetDevice(ctx->device));
     if (int rc = upload(ctx, ctx->prop, property, 1)) return rc;
+    ctx->ecell_valid = false;
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->prop_node0 = property[0];
     ctx->prop_node0_valid = true;
@@ -776,6 +804,7 @@ int petto_dev_set_lame(petto_ctx* ctx, const double* lambda, const double* mu) {
     // positivity of both Lame fields (state_solver.hpp:295-297), lambda staged in the residual scratch
     if (int rc = upload(ctx, ctx->r, lambda, 1)) return rc;
     if (int rc = upload(ctx, ctx->prop, mu, 1)) return rc;
+    ctx->ecell_valid = false;
     CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
     k_check_positive<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->r, 1.0, 1.0,
                                                                             &ctx->status->flags);
@@ -1141,6 +1170,7 @@ int petto_dev_interpolate(petto_ctx* ctx, double* property_out) {
     if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
     const long long n = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nzs;
     k_interpolate<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->g, design_params(ctx), ctx->phases, ctx->prop);
+    ctx->ecell_valid = false;
     ctx->launches++;
     CKL();
     ctx->prop_node0_valid = false;

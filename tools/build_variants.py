@@ -26,14 +26,15 @@ def one(spec):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         return f"{name}: FAILED\n{r.stderr[-2000:]}"
-    m = re.search(r"k_elastic3d_fastILi1E.*?\n(.*?spill.*?)\n.*?Used (\d+) registers", r.stderr, re.S)
+    m = re.search(r"k_elastic3d_(?:fast|shift)ILi1E.*?\n(.*?spill.*?)\n.*?Used (\d+) registers", r.stderr, re.S)
     return f"{name}: {m.group(2)} regs, {m.group(1).strip()}" if m else f"{name}: built"
 
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    for f in os.listdir(OUT):
-        os.remove(os.path.join(OUT, f))
+    for f in os.listdir(OUT):  # keep_* libraries (a frozen baseline) survive rebuilds
+        if not f.startswith("libpetto_keep_"):
+            os.remove(os.path.join(OUT, f))
     with ThreadPoolExecutor(4) as ex:
         for line in ex.map(one, sys.argv[1:]):
             print(line)
