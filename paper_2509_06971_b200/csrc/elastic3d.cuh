@@ -78,7 +78,7 @@ constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][ZP][6]
 constexpr int OFF_X = OFF_Y + 2 * NWARP * YS * 8;           // [2][LMAX][NWARP][3] f64
 constexpr int OFF_O = OFF_X + 2 * LMAX * NWARP * 3 * 8;     // [2][OUT_ELEMS] f64
 constexpr int OFF_BAR = OFF_O + 2 * OUT_ELEMS * 8;          // [S] full
-constexpr int OFF_RED = OFF_BAR + S * 8;                    // [NWARP] f64
+constexpr int OFF_RED = OFF_BAR + S * 8;                    // [2 NWARP] f64
 constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
 constexpr int SMEM_BYTES = OFF_CUR + 128;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -546,6 +546,232 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (P.partials) P.partials[blockIdx.x] = sum;
     }
     if (E3_EXPERIMENT == 0 && bad && l == 0) mark_bad(P.status, P.step);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised variant (E3_WS): 16 warps per CTA.  Warps 0-7 ("cell warps",
+// rows j0-1 .. j0+6, 184 registers each via setmaxnreg) stream the forward
+// butterflies and the cell stiffness of task q; warps 9-15 ("node warps", rows
+// j0 .. j0+6, 72 registers) assemble and update the nodes of task q-1 at the
+// same time; warp 8 is the producer (TMA loads, output stores).  A cell warp
+// hands its row-j face sums to the node warp of the same row through tensor
+// memory (same TMEM lane quarter: warp % 4) and its row-(j+1) shares through
+// shared memory; one CTA barrier per task separates the phases.  The FP64-heavy
+// cell work and the latency-bound node work of different tasks overlap on every
+// scheduler.
+#ifndef E3_WS
+#define E3_WS 1
+#endif
+constexpr int WS_THREADS = 2 * NTHREADS;
+constexpr uint32_t REG_CELL = 184, REG_NODE = 72;  // 8 x 184 + 8 x 72 = 2048 = 64K / 32
+constexpr uint32_t TMEM_COLS = 128;                // [2 warp halves][2 parities][32 columns]
+constexpr int OFF_TMEM = OFF_CUR + 64;             // TMEM base address (u32)
+static_assert(NWARP == 8, "warp roles assume 8 cell warps");
+
+// Calls f(own, s, t, ka, kc, two) for every task of the CTA in order: per x tile
+// the prologue (own = false, cell plane ka-1), then the owned two-plane tasks.
+template <class F>
+__device__ __forceinline__ void walk(const Params& P, F&& f) {
+    const Geo& g = P.g;
+    for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
+        const int s = item % P.nstrips;
+        const int ka = g.kb + (item / P.nstrips) * P.chunk;
+        const int kb = min(ka + P.chunk, g.ke);
+        for (int t = 0; t < P.ntx; ++t) {
+            f(false, s, t, ka, ka - 1, false);
+            for (int kc = ka; kc < kb; kc += ZP) f(true, s, t, ka, kc, kc + 1 < kb);
+        }
+    }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    k_elastic3d_ws(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const Geo& g = P.g;
+    if (skip_step(P.status, P.step, P.nsteps)) return;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    double* sY = reinterpret_cast<double*>(smem + OFF_Y);
+    double* sX = reinterpret_cast<double*>(smem + OFF_X);
+    Cursor* pc = reinterpret_cast<Cursor*>(smem + OFF_CUR);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    if (w == 0) tmem_alloc(tslot, TMEM_COLS);
+    if (w == 8 && l == 0) {
+        prefetch_tmap(&M.u);
+        prefetch_tmap(&M.c);
+        prefetch_tmap(&M.p);
+        prefetch_tmap(&M.m);
+        prefetch_tmap(&M.o2);
+        prefetch_tmap(&M.o1);
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        pc->item = blockIdx.x;
+        pc->t = 0;
+        pc->kk = 0;
+        pc->set(P);
+        for (int s = 0; s < S - 1 && pc->valid; ++s) {
+            issue<FORM>(P, *pc, smem, bars, s, M);
+            pc->next(P);
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = *tslot;
+    double rsq = 0.0;
+    unsigned bad = 0;
+
+    if (w < NWARP) {
+        // ------------------------------------------------------------ cell warps
+        regs_grow<REG_CELL>();
+        double Bc[4][3], top[4][3];
+        uint32_t st = 0, phase = 0, q = 0;
+        const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (w >> 2) * 64;
+        walk(P, [&](bool own, int, int, int, int, bool two) {
+            mbar_wait(&bars[st], phase);
+            const unsigned char* sb = smem + st * STAGE_BYTES;
+            const double* sc = reinterpret_cast<const double*>(sb + OFF_C) + w * 32 + l;
+            if (!own) {  // prologue: node planes ka-1, ka and cell plane ka-1
+                double B0[4][3], Yd[2][3];
+                forward(sb, 0, w, l, B0);
+                forward(sb, 1, w, l, Bc);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+                cell<false>(P, B0, Bc, sc[0], top, Yd, nullptr);
+            } else {
+                double* sYw = sY + (q & 1) * (NWARP * YS) + w * YS + l;
+                double B1[4][3], Y0[2][3], Y1[2][3];
+                forward(sb, 0, w, l, B1);
+                cell<true>(P, Bc, B1, sc[0], top, Y0, sYw);
+                if (two) {
+                    forward(sb, 1, w, l, Bc);
+                    cell<true>(P, B1, Bc, sc[NWARP * 32], top, Y1, sYw + 6 * 32);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) Y1[k / 3][k % 3] = 0.0;
+                }
+                if (w > 0) {  // the y-halo row's own sums are not needed
+                    const uint32_t ta = tq + (q & 1) * 32;
+                    tmem_st4(ta, Y0[0][0], Y0[0][1], Y0[0][2], Y0[1][0]);
+                    tmem_st4(ta + 8, Y0[1][1], Y0[1][2], Y1[0][0], Y1[0][1]);
+                    tmem_st4(ta + 16, Y1[0][2], Y1[1][0], Y1[1][1], Y1[1][2]);
+                    tmem_wait_st();
+                }
+            }
+            tmem_fence_before();
+            __syncthreads();  // task q's shares and sums are complete
+            ++q;
+            if (++st == S) {
+                st = 0;
+                phase ^= 1u;
+            }
+        });
+        __syncthreads();  // the node warps' last task
+    } else if (w == NWARP) {
+        // ------------------------------------------------------------- producer
+        regs_shrink<REG_NODE>();
+        uint32_t st = 0;
+        int ob = 0, pend = 0, px = 0, py = 0, pz = 0, pb = 0;
+        walk(P, [&](bool own, int s, int t, int, int kc, bool two) {
+            __syncthreads();  // cell warps done with task q, node warps with task q-1
+            if (l == 0) {
+                if (pc->valid) {
+                    issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
+                    pc->next(P);
+                }
+                if (pend) {  // the node warps' output of task q-1
+                    const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pb * OUT_ELEMS;
+                    tma_store_4d(pend == 2 ? &M.o2 : &M.o1, src, px, py, pz, 0);
+                    bulk_commit();
+                    bulk_wait_read();  // its buffer is rewritten two tasks later
+                }
+            }
+            pend = own ? (two ? 2 : 1) : 0;
+            px = t * 32;
+            py = s * W;
+            pz = kc - g.ks0;
+            pb = ob;
+            if (own) ob ^= 1;
+            if (++st == S) st = 0;
+        });
+        __syncthreads();
+        if (l == 0) {
+            if (pend) {
+                const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pb * OUT_ELEMS;
+                tma_store_4d(pend == 2 ? &M.o2 : &M.o1, src, px, py, pz, 0);
+                bulk_commit();
+            }
+            bulk_wait_all();
+        }
+    } else {
+        // ------------------------------------------------------------ node warps
+        regs_shrink<REG_NODE>();
+        const int v = w - NWARP;  // row j0-1+v, v = 1..7
+        double ucar[3] = {0.0, 0.0, 0.0};
+        uint32_t st = 0, q = 0;
+        int ob = 0;
+        const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
+        walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
+            __syncthreads();  // the cell warps finished task q
+            tmem_fence_after();
+            const unsigned char* sb = smem + st * STAGE_BYTES;
+            const double* su = reinterpret_cast<const double*>(sb + OFF_U) + v * BOXX + l;  // plane 0, row v
+            if (own) {
+                Tile T;
+                T.t = t;
+                const int i = t * 32 + l, j = s * W - 1 + v;
+                T.upd = i < g.nx && j < g.ny;
+                const int ends = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
+                T.ninv = -P.inv_base * (double)(1 << ends);
+                T.ninv_end = 2.0 * T.ninv;
+                T.node0 = (long long)j * g.px + i;
+                T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + v * 3;
+                T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + v * 3;
+                double Yv[12];
+                tmem_ld12(tq + (q & 1) * 32, Yv);
+                const double Y0[2][3] = {{Yv[0], Yv[1], Yv[2]}, {Yv[3], Yv[4], Yv[5]}};
+                const double Y1[2][3] = {{Yv[6], Yv[7], Yv[8]}, {Yv[9], Yv[10], Yv[11]}};
+                const double* below = sY + (q & 1) * (NWARP * YS) + (v - 1) * YS + l;
+                const unsigned char* mk = sb + OFF_M + (v - 1) * 32 + l;
+                const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (v - 1) * 32 + l;
+                double* out = reinterpret_cast<double*>(smem + OFF_O) + ob * OUT_ELEMS + (v - 1) * 32 + l;
+                const int ocs = two ? ZP * W * 32 : W * 32;
+                node<FORM>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], out, ocs, rsq, bad);
+                if (two) {
+                    double u1[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
+                    node<FORM>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32],
+                               out + W * 32, ocs, rsq, bad);
+                }
+                fence_proxy_async();  // output tile -> the producer's TMA store
+                ob ^= 1;
+            }
+            // u_n of the next task's first node plane (stage plane 1)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE + UROWS * BOXX];
+            ++q;
+            if (++st == S) st = 0;
+        });
+        __syncthreads();
+    }
+
+    // CTA reduction of r^2 (fixed order) and the non-finite flag
+    double* red = reinterpret_cast<double*>(smem + OFF_RED);
+    rsq = warp_sum(rsq);
+    bad = __any_sync(0xffffffffu, bad);
+    if (l == 0) red[w] = rsq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int k = 0; k < 2 * NWARP; ++k) sum += red[k];
+        if (P.partials) P.partials[blockIdx.x] = sum;
+    }
+    if (bad && l == 0) mark_bad(P.status, P.step);
+    if (w == 0) tmem_dealloc(tbase, TMEM_COLS);
 }
 
 // Cell modulus of every stored cell (i, j, k), k = ks0 + kl: the operator scale

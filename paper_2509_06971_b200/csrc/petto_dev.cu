@@ -346,12 +346,18 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             M.o1 = ctx->tO1[ob];
             timing_begin(ctx, ev);
             const int smem = e3::SMEM_BYTES;
+#if E3_WS
+#define E3_LAUNCH(F) e3::k_elastic3d_ws<F><<<grid, e3::WS_THREADS, smem, ctx->stream>>>(P, M)
+#else
+#define E3_LAUNCH(F) e3::k_elastic3d_fast<F><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M)
+#endif
             switch (k.form) {
-                case 0: e3::k_elastic3d_fast<0><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
-                case 1: e3::k_elastic3d_fast<1><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
-                case 2: e3::k_elastic3d_fast<2><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
-                default: e3::k_elastic3d_fast<3><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M); break;
+                case 0: E3_LAUNCH(0); break;
+                case 1: E3_LAUNCH(1); break;
+                case 2: E3_LAUNCH(2); break;
+                default: E3_LAUNCH(3); break;
             }
+#undef E3_LAUNCH
             timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
             ctx->launches++;
             CKL();
@@ -632,10 +638,15 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess)
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (cudaFuncSetAttribute(e3::k_elastic3d_fast<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_fast<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_fast<2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_fast<3>, smattr, e3::SMEM_BYTES) != cudaSuccess)
+#if E3_WS
+#define E3_KERNEL e3::k_elastic3d_ws
+#else
+#define E3_KERNEL e3::k_elastic3d_fast
+#endif
+    if (cudaFuncSetAttribute(E3_KERNEL<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");
