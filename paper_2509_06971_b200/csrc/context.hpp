@@ -58,11 +58,11 @@ struct petto_ctx {
     petto_b200::DeviceStatus* status_h = nullptr; // pinned host mirror
 
     // fused 3D kernel: per-cell modulus (recomputed after a property change) and
-    // TMA descriptors (outputs: the three state buffers and the residual scratch)
+    // TMA descriptors
     double* ecell = nullptr;
     bool ecell_valid = false;
     double ecell_scale = 0.0;
-    CUtensorMap tU[3], tP[3], tC, tM, tO2[4], tO1[4];
+    CUtensorMap tU[3], tP[3], tC, tM;
     bool tmaps = false;
 
     // design subsystem

@@ -20,9 +20,7 @@
 //     the top-face contributions (12 doubles) in registers;
 //   * node planes arrive by TMA (cp.async.bulk.tensor, zero-filled outside the
 //     grid) into an S-stage shared-memory ring guarded by mbarriers, issued S-1
-//     tasks ahead by one elected thread; the updated nodes leave through a
-//     double-buffered shared tile and a TMA tensor store issued at the next
-//     barrier, so no thread waits on its global stores;
+//     tasks ahead by one elected thread;
 //   * x-neighbour contributions travel by warp shuffle, y-neighbour ones through
 //     a double-buffered shared tile (one CTA barrier per task, i.e. per ZP
 //     planes), and the previous x-tile's last column through a small shared
@@ -72,12 +70,10 @@ constexpr uint32_t BYTES_M = ZP * W * 32;
 constexpr int USTRIDE = ZP * UROWS * BOXX;  // component stride of the U tile
 constexpr int PSTRIDE = ZP * W * 32;        // component stride of the P tile
 constexpr int YS = ZP * 6 * 32;             // one warp's y shares of one task
-constexpr int OUT_ELEMS = 3 * ZP * W * 32;  // one output tile [3][ZP][W][32] (tail: [3][1][W][32])
 
 constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][ZP][6][32] f64
 constexpr int OFF_X = OFF_Y + 2 * NWARP * YS * 8;           // [2][LMAX][NWARP][3] f64
-constexpr int OFF_O = OFF_X + 2 * LMAX * NWARP * 3 * 8;     // [2][OUT_ELEMS] f64
-constexpr int OFF_BAR = OFF_O + 2 * OUT_ELEMS * 8;          // [S] full
+constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] full
 constexpr int OFF_RED = OFF_BAR + S * 8;                    // [2 NWARP] f64
 constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
 constexpr int SMEM_BYTES = OFF_CUR + 128;
@@ -89,6 +85,7 @@ struct Params {
     double inv_base;   // 1 / (hx hy hz)
     // update coefficients: APT u' = c1 u - c2 u_prev + c3 r; PT u' = u + dt r
     double c1, c2, c3, dt;
+    double* next;      // output field (may alias the previous iterate)
     const double* aux; // pinned values / loads (3 x Ns)
     double* partials;  // per-CTA sum of r^2 over unconstrained entries (nullable)
     DeviceStatus* status;
@@ -106,8 +103,6 @@ struct Maps {
     CUtensorMap c;     // cell modulus: box [ZP][NWARP][32]
     CUtensorMap p;     // previous iterate: box [3][ZP][W][32]
     CUtensorMap m;     // node mask: box [ZP][W][32]
-    CUtensorMap o2;    // output: box [3][ZP][W][32]
-    CUtensorMap o1;    // output, one plane: box [3][1][W][32]
 };
 
 // Producer cursor over the CTA's task sequence: items (b, b+grid, ...), x tiles,
@@ -168,16 +163,6 @@ struct Tile {
     long long node0;     // lidx(i, j, 0) (loads and pinned values)
     double* xw;          // x-halo out (lane 31) / in (lane 0)
     const double* xr;
-};
-
-struct Pipe {
-    unsigned char* smem;
-    uint64_t* bars;
-    int st, q;
-    uint32_t phase;
-    // output tile waiting for the next barrier: planes (0 none, 1, 2), origin, buffer
-    int pst, px, py, pz, pbuf;
-    int ob;              // buffer of the next owned task's output tile
 };
 
 // forward x/y butterflies of stage plane z for cell (i, j): B[sx + 2 sy][c]
@@ -291,45 +276,12 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     }
 }
 
-// Barrier after the y shares are written.  Then the producer refills the stage of
-// the previous task (every warp is past its last read of it) and issues the TMA
-// store of the output tile finished before the barrier; before the barrier it
-// waits until the store issued at the previous barrier has read its buffer (the
-// buffer the coming node phase overwrites).
-template <int FORM>
-__device__ __forceinline__ void end_task(const Params& P, Pipe& pp, Cursor* pc, const Maps& T) {
-    fence_proxy_async();  // this thread's output-tile writes -> async proxy
-    if (threadIdx.x == 0) bulk_wait_read();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (pc->valid) {
-            issue<FORM>(P, *pc, pp.smem, pp.bars, pp.st == 0 ? S - 1 : pp.st - 1, T);
-            pc->next(P);
-        }
-        if (pp.pst && E3_EXPERIMENT != 1) {
-            const double* src = reinterpret_cast<const double*>(pp.smem + OFF_O) + pp.pbuf * OUT_ELEMS;
-            tma_store_4d(pp.pst == 2 ? &T.o2 : &T.o1, src, pp.px, pp.py, pp.pz, 0);
-            bulk_commit();
-        }
-    }
-    pp.pst = 0;
-}
-
-__device__ __forceinline__ void advance(Pipe& pp) {
-    ++pp.q;
-    if (++pp.st == S) {
-        pp.st = 0;
-        pp.phase ^= 1u;
-    }
-}
-
 // Node (i, j, kc): edge sums with warp w-1's shares, inverse x butterflies (x-halo
-// for lane 0), then the residual, the update and the write into the output tile
-// (component stride ocs).  u_n arrives in u.
+// for lane 0), then the residual, the update and the store.  u_n arrives in u.
 template <int FORM>
 __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int zi, const double (&Yj)[2][3],
                                      const double* below, const double (&u)[3], const double* sp,
-                                     unsigned char mk, double* out, int ocs, double& rsq, unsigned& bad) {
+                                     unsigned char mk, double& rsq, unsigned& bad) {
     const int l = threadIdx.x & 31;
     const Geo& g = P.g;
     double Xi[3], Xn[3];
@@ -384,186 +336,31 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
     }
     // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
     unsigned ex = 0;
+    double* dst = P.next + T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
-        out[c * ocs] = nv[c];
+        dst[c * g.Ns] = nv[c];
     }
     bad |= ex;
 }
 
-// Owned node planes kc (and kc+1 when two): forward of node planes kc+1, kc+2,
-// cell planes kc, kc+1, one barrier, then the node planes into the output tile.
-// On entry Bc holds the butterflies of node plane kc and ucar its u_n; on exit
-// both describe kc+2.
-template <int FORM>
-__device__ __forceinline__ void own_task(const Params& P, Pipe& pp, Cursor* pc, const Maps& M, const Tile& T,
-                                         int s, int kc, int zi, bool two, double (&Bc)[4][3], double (&top)[4][3],
-                                         double (&ucar)[3], double& rsq, unsigned& bad, double* sY) {
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const Geo& g = P.g;
-    mbar_wait(&pp.bars[pp.st], pp.phase);
-    const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
-    double* sYt = sY + (pp.q & 1) * (NWARP * YS);
-    double* sYw = sYt + w * YS + l;
-    const double* sc = reinterpret_cast<const double*>(sb + OFF_C) + w * 32 + l;
-    double B1[4][3], Y0[2][3], Y1[2][3];
-    forward(sb, 0, w, l, B1);
-    cell<true>(P, Bc, B1, sc[0], top, Y0, sYw);
-    if (two) {  // warp-uniform
-        forward(sb, 1, w, l, Bc);
-        cell<true>(P, B1, Bc, sc[NWARP * 32], top, Y1, sYw + 6 * 32);
-    }
-    end_task<FORM>(P, pp, pc, M);
-    const int ob = pp.ob;
-    pp.ob ^= 1;
-    pp.pst = two ? 2 : 1;
-    pp.px = T.t * 32;
-    pp.py = s * W;
-    pp.pz = kc - g.ks0;
-    pp.pbuf = ob;
-    if (w > 0) {  // warp-uniform: warp 0 (the y-halo row) only emits shares
-        const double* below = sYt + (w - 1) * YS + l;
-        const unsigned char* mk = sb + OFF_M + (w - 1) * 32 + l;
-        const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (w - 1) * 32 + l;
-        const double* su = reinterpret_cast<const double*>(sb + OFF_U) + w * BOXX + l;  // node plane kc+1
-        double* out = reinterpret_cast<double*>(pp.smem + OFF_O) + ob * OUT_ELEMS + (w - 1) * 32 + l;
-        const int ocs = two ? ZP * W * 32 : W * 32;
-        node<FORM>(P, T, kc, zi, Y0, below, ucar, sp, mk[0], out, ocs, rsq, bad);
-        if (two) {
-            double u1[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
-            node<FORM>(P, T, kc + 1, zi + 1, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32], out + W * 32, ocs,
-                       rsq, bad);
-        }
-        // node plane kc+2 feeds the next task (this stage is only recycled after
-        // the next task's barrier)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE + UROWS * BOXX];
-    }
-    advance(pp);
-}
-
-template <int FORM>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const Geo& g = P.g;
-    if (skip_step(P.status, P.step, P.nsteps)) return;
-    Pipe pp{smem, reinterpret_cast<uint64_t*>(smem + OFF_BAR), 0, 0, 0u, 0, 0, 0, 0, 0, 0};
-    double* sY = reinterpret_cast<double*>(smem + OFF_Y);
-    double* sX = reinterpret_cast<double*>(smem + OFF_X);
-    Cursor* pc = reinterpret_cast<Cursor*>(smem + OFF_CUR);
-    if (E3_EXPERIMENT == 1)  // compute-only runs read a zeroed ring
-        for (int b = threadIdx.x; b < S * STAGE_BYTES / 4; b += NTHREADS) reinterpret_cast<uint32_t*>(smem)[b] = 0u;
-    if (threadIdx.x == 0) {
-        prefetch_tmap(&M.u);
-        prefetch_tmap(&M.c);
-        prefetch_tmap(&M.p);
-        prefetch_tmap(&M.m);
-        prefetch_tmap(&M.o2);
-        prefetch_tmap(&M.o1);
-        for (int s = 0; s < S; ++s) mbar_init(&pp.bars[s], 1);  // the producer's expect_tx + TMA bytes
-        fence_mbar_init();
-        pc->item = blockIdx.x;
-        pc->t = 0;
-        pc->kk = 0;
-        pc->set(P);
-        for (int s = 0; s < S - 1 && pc->valid; ++s) {
-            issue<FORM>(P, *pc, smem, pp.bars, s, M);
-            pc->next(P);
-        }
-    }
-    __syncthreads();
-
-    double Bc[4][3], top[4][3], ucar[3] = {0.0, 0.0, 0.0};
-    double rsq = 0.0;
-    unsigned bad = 0;
-    for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
-        const int s = item % P.nstrips;
-        const int ka = g.kb + (item / P.nstrips) * P.chunk;
-        const int kb = min(ka + P.chunk, g.ke);
-        for (int t = 0; t < P.ntx; ++t) {
-            Tile T;
-            T.t = t;
-            const int i = t * 32 + l, j = s * W - 1 + w;
-            T.upd = w >= 1 && i < g.nx && j < g.ny;
-            const int ends = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
-            T.ninv = -P.inv_base * (double)(1 << ends);
-            T.ninv_end = 2.0 * T.ninv;
-            T.node0 = (long long)max(j, 0) * g.px + i;
-            T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + w * 3;
-            T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + w * 3;
-
-            // prologue: butterflies of node planes ka-1 and ka, cell plane ka-1
-            // (its top face feeds node plane ka)
-            {
-                mbar_wait(&pp.bars[pp.st], pp.phase);
-                const unsigned char* sb = pp.smem + pp.st * STAGE_BYTES;
-                double B0[4][3], Yd[2][3];
-                forward(sb, 0, w, l, B0);
-                forward(sb, 1, w, l, Bc);
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
-                const double ec = reinterpret_cast<const double*>(sb + OFF_C)[w * 32 + l];
-                cell<false>(P, B0, Bc, ec, top, Yd, nullptr);
-                const double* su = reinterpret_cast<const double*>(sb + OFF_U) + (UROWS + w) * BOXX + l;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE];
-                end_task<FORM>(P, pp, pc, M);
-                advance(pp);
-            }
-            for (int kc = ka; kc < kb; kc += ZP)
-                own_task<FORM>(P, pp, pc, M, T, s, kc, kc - ka, kc + 1 < kb, Bc, top, ucar, rsq, bad, sY);
-        }
-    }
-    // the last output tile
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (pp.pst && E3_EXPERIMENT != 1) {
-            const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pp.pbuf * OUT_ELEMS;
-            tma_store_4d(pp.pst == 2 ? &M.o2 : &M.o1, src, pp.px, pp.py, pp.pz, 0);
-            bulk_commit();
-        }
-        bulk_wait_all();
-    }
-
-    // CTA reduction of r^2 (fixed order) and the non-finite flag
-    double* red = reinterpret_cast<double*>(smem + OFF_RED);
-    rsq = warp_sum(rsq);
-    bad = __any_sync(0xffffffffu, bad);
-    __syncthreads();
-    if (l == 0) red[w] = rsq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double sum = 0.0;
-        for (int k = 0; k < NWARP; ++k) sum += red[k];
-        if (P.partials) P.partials[blockIdx.x] = sum;
-    }
-    if (E3_EXPERIMENT == 0 && bad && l == 0) mark_bad(P.status, P.step);
-}
-
 // ---------------------------------------------------------------------------
-// Warp-specialised variant (E3_WS): 16 warps per CTA.  Warps 0-7 ("cell warps",
+// The kernel is warp-specialised: 16 warps per CTA.  Warps 0-7 ("cell warps",
 // rows j0-1 .. j0+6, 184 registers each via setmaxnreg) stream the forward
 // butterflies and the cell stiffness of task q; warps 9-15 ("node warps", rows
 // j0 .. j0+6, 72 registers) assemble and update the nodes of task q-1 at the
-// same time; warp 8 is the producer (TMA loads, output stores).  A cell warp
+// same time; warp 8 is the producer (TMA loads).  A cell warp
 // hands its row-j face sums to the node warp of the same row through tensor
 // memory (same TMEM lane quarter: warp % 4) and its row-(j+1) shares through
 // shared memory; one CTA barrier per task separates the phases.  The FP64-heavy
 // cell work and the latency-bound node work of different tasks overlap on every
 // scheduler.
-#ifndef E3_WS
-#define E3_WS 1
-#endif
 constexpr int WS_THREADS = 2 * NTHREADS;
-constexpr uint32_t REG_CELL = 184, REG_NODE = 72;  // 8 x 184 + 8 x 72 = 2048 = 64K / 32
+#ifndef E3_REG_CELL
+#define E3_REG_CELL 184
+#endif
+constexpr uint32_t REG_CELL = E3_REG_CELL, REG_NODE = 256 - E3_REG_CELL;  // 8 (cell + node) = 2048 = 64K / 32
 constexpr uint32_t TMEM_COLS = 128;                // [2 warp halves][2 parities][32 columns]
 constexpr int OFF_TMEM = OFF_CUR + 64;             // TMEM base address (u32)
 static_assert(NWARP == 8, "warp roles assume 8 cell warps");
@@ -586,7 +383,7 @@ __device__ __forceinline__ void walk(const Params& P, F&& f) {
 
 template <int FORM>
 __global__ void __launch_bounds__(WS_THREADS, 1)
-    k_elastic3d_ws(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
+    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
@@ -602,8 +399,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         prefetch_tmap(&M.c);
         prefetch_tmap(&M.p);
         prefetch_tmap(&M.m);
-        prefetch_tmap(&M.o2);
-        prefetch_tmap(&M.o1);
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         pc->item = blockIdx.x;
@@ -674,45 +469,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // ------------------------------------------------------------- producer
         regs_shrink<REG_NODE>();
         uint32_t st = 0;
-        int ob = 0, pend = 0, px = 0, py = 0, pz = 0, pb = 0;
-        walk(P, [&](bool own, int s, int t, int, int kc, bool two) {
+        walk(P, [&](bool, int, int, int, int, bool) {
             __syncthreads();  // cell warps done with task q, node warps with task q-1
-            if (l == 0) {
-                if (pc->valid) {
-                    issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
-                    pc->next(P);
-                }
-                if (pend) {  // the node warps' output of task q-1
-                    const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pb * OUT_ELEMS;
-                    tma_store_4d(pend == 2 ? &M.o2 : &M.o1, src, px, py, pz, 0);
-                    bulk_commit();
-                    bulk_wait_read();  // its buffer is rewritten two tasks later
-                }
+            if (l == 0 && pc->valid) {  // refill the stage of task q-1
+                issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
+                pc->next(P);
             }
-            pend = own ? (two ? 2 : 1) : 0;
-            px = t * 32;
-            py = s * W;
-            pz = kc - g.ks0;
-            pb = ob;
-            if (own) ob ^= 1;
             if (++st == S) st = 0;
         });
         __syncthreads();
-        if (l == 0) {
-            if (pend) {
-                const double* src = reinterpret_cast<const double*>(smem + OFF_O) + pb * OUT_ELEMS;
-                tma_store_4d(pend == 2 ? &M.o2 : &M.o1, src, px, py, pz, 0);
-                bulk_commit();
-            }
-            bulk_wait_all();
-        }
     } else {
         // ------------------------------------------------------------ node warps
         regs_shrink<REG_NODE>();
         const int v = w - NWARP;  // row j0-1+v, v = 1..7
         double ucar[3] = {0.0, 0.0, 0.0};
         uint32_t st = 0, q = 0;
-        int ob = 0;
         const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
         walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
             __syncthreads();  // the cell warps finished task q
@@ -737,18 +508,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 const double* below = sY + (q & 1) * (NWARP * YS) + (v - 1) * YS + l;
                 const unsigned char* mk = sb + OFF_M + (v - 1) * 32 + l;
                 const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (v - 1) * 32 + l;
-                double* out = reinterpret_cast<double*>(smem + OFF_O) + ob * OUT_ELEMS + (v - 1) * 32 + l;
-                const int ocs = two ? ZP * W * 32 : W * 32;
-                node<FORM>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], out, ocs, rsq, bad);
+                node<FORM>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], rsq, bad);
                 if (two) {
                     double u1[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
-                    node<FORM>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32],
-                               out + W * 32, ocs, rsq, bad);
+                    node<FORM>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32], rsq,
+                               bad);
                 }
-                fence_proxy_async();  // output tile -> the producer's TMA store
-                ob ^= 1;
             }
             // u_n of the next task's first node plane (stage plane 1)
 #pragma unroll

@@ -127,19 +127,15 @@ int make_tmaps(petto_ctx* ctx) {
     const cuuint64_t s4[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8, (cuuint64_t)g.Ns * 8};
     const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, e3::ZP, 3};
     const cuuint32_t boxP[4] = {32, e3::W, e3::ZP, 3};
-    const cuuint32_t boxO1[4] = {32, e3::W, 1, 3};
     const cuuint32_t one[4] = {1, 1, 1, 1};
     auto map4 = [&](CUtensorMap* m, double* base, const cuuint32_t* box) {
         return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, d4, s4, box, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
-    for (int b = 0; b < 4; ++b) {
-        double* base = b < 3 ? ctx->st[b] : ctx->r;
-        if ((b < 3 && (!map4(&ctx->tU[b], base, boxU) || !map4(&ctx->tP[b], base, boxP))) ||
-            !map4(&ctx->tO2[b], base, boxP) || !map4(&ctx->tO1[b], base, boxO1))
+    for (int b = 0; b < 3; ++b)
+        if (!map4(&ctx->tU[b], ctx->st[b], boxU) || !map4(&ctx->tP[b], ctx->st[b], boxP))
             return fail(ctx, PETTO_ERROR, "tensor map (state) encode failed");
-    }
     const cuuint64_t d3[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs};
     const cuuint64_t s3[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8};
     const cuuint32_t boxC[3] = {32, e3::NWARP, e3::ZP};
@@ -316,6 +312,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
                 P.c3 = k.a * k.inv;
             }
             P.dt = k.dt;
+            P.next = next;
             P.aux = ctx->aux;
             P.partials = partials;
             P.status = ctx->status;
@@ -332,25 +329,14 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             P.nitems = P.nstrips * ((nzo + P.chunk - 1) / P.chunk);
             grid = std::min(grid, P.nitems);
             if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
-            int ob = -1;
-            for (int b = 0; b < 3; ++b)
-                if (next == ctx->st[b]) ob = b;
-            if (next == ctx->r) ob = 3;
-            if (ob < 0) return fail(ctx, PETTO_ERROR, "fused 3D step: output is not a context buffer");
             e3::Maps M;
             M.u = ctx->tU[cur];
             M.c = ctx->tC;
             M.p = ctx->tP[prev];
             M.m = ctx->tM;
-            M.o2 = ctx->tO2[ob];
-            M.o1 = ctx->tO1[ob];
             timing_begin(ctx, ev);
             const int smem = e3::SMEM_BYTES;
-#if E3_WS
-#define E3_LAUNCH(F) e3::k_elastic3d_ws<F><<<grid, e3::WS_THREADS, smem, ctx->stream>>>(P, M)
-#else
-#define E3_LAUNCH(F) e3::k_elastic3d_fast<F><<<grid, e3::NTHREADS, smem, ctx->stream>>>(P, M)
-#endif
+#define E3_LAUNCH(F) e3::k_elastic3d_fast<F><<<grid, e3::WS_THREADS, smem, ctx->stream>>>(P, M)
             switch (k.form) {
                 case 0: E3_LAUNCH(0); break;
                 case 1: E3_LAUNCH(1); break;
@@ -638,11 +624,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess)
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-#if E3_WS
-#define E3_KERNEL e3::k_elastic3d_ws
-#else
 #define E3_KERNEL e3::k_elastic3d_fast
-#endif
     if (cudaFuncSetAttribute(E3_KERNEL<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(E3_KERNEL<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(E3_KERNEL<2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
