@@ -45,6 +45,15 @@ namespace e3 {
 #ifndef E3_S
 #define E3_S 4
 #endif
+#ifndef E3_PACE
+#define E3_PACE 0  // strip pacing slack in tasks (0: off)
+#endif
+#ifndef E3_PACE_SLEEP
+#define E3_PACE_SLEEP 0
+#endif
+#ifndef E3_SMID_MAP
+#define E3_SMID_MAP 1
+#endif
 #ifndef E3_EXPERIMENT
 #define E3_EXPERIMENT 0  // 1: no TMA traffic (compute only), 2: no cell math (traffic only)
 #endif
@@ -94,8 +103,27 @@ struct Params {
     int nstrips;       // y strips of W rows
     int chunk;         // owned planes per z chunk (<= LMAX)
     int nitems;        // nstrips * chunks
+    // pacing of neighbouring strips (null: off): CTA b publishes the number of
+    // task loads it has issued in progress[b] (offset by epoch) and issues task x
+    // only once the CTAs of the strips above and below have issued task x - pace,
+    // so a halo row is read twice within a few tasks and the second read hits L2
+    unsigned long long* progress;
+    unsigned long long epoch;
+    int pace;
+    int smid_map;      // work items by SM id (see vblock)
 };
+#ifndef E3_CONST_KH
+#define E3_CONST_KH 0
+#endif
+
+// modal stiffness operands: kernel parameters, or (E3_CONST_KH) a __constant__
+// bank refreshed on the launching stream before each launch
+__constant__ double c_kh[48];
+#if E3_CONST_KH
+#define KH c_kh
+#else
 #define KH P.kh
+#endif
 
 // The tensor maps of one launch (kernel parameters, 64-byte aligned).
 struct Maps {
@@ -109,7 +137,7 @@ struct Maps {
 // tasks kk = 0 (prologue: node planes ka-1, ka) and kk >= 1 (owned planes
 // kc = ka + ZP (kk-1) ..., loading node planes kc+1 .. kc+ZP).
 struct Cursor {
-    int item, t, kk, s, ka, ntask;
+    int item, t, kk, s, ka, ntask, n;
     bool valid;
     __device__ void set(const Params& P) {
         valid = item < P.nitems;
@@ -119,6 +147,7 @@ struct Cursor {
         ntask = 1 + (min(P.chunk, P.g.ke - ka) + ZP - 1) / ZP;
     }
     __device__ void next(const Params& P) {
+        ++n;
         if (++kk == ntask) {
             kk = 0;
             if (++t == P.ntx) {
@@ -129,6 +158,49 @@ struct Cursor {
         }
     }
 };
+
+// Work-item index of this CTA.  With one item per SM (a cooperative launch of
+// exactly one CTA per SM) items follow the SM id, so consecutive strips -- which
+// read each other's halo rows -- run on neighbouring SMs of one die and share its
+// L2; otherwise the block index.
+__device__ __forceinline__ int vblock(const Params& P) {
+    if (P.smid_map) {
+        unsigned s;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+        return (int)s;
+    }
+    return blockIdx.x;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Producer side of the strip pacing: wait until the neighbouring strips' CTAs
+// have issued task n - pace (one item per CTA; neighbours share the z chunk).
+// Relaxed accesses: the counters only pace the loads, they publish no data (a
+// release store would also wait for this thread's in-flight TMA loads).
+__device__ __forceinline__ void pace_wait(const Params& P, int n) {
+    if (!P.progress || n < P.pace) return;
+    const unsigned long long target = P.epoch + (unsigned long long)(n - P.pace);
+    const int b = vblock(P), s = b % P.nstrips;
+    if (s > 0)
+        while (ld_relaxed(P.progress + b - 1) < target) {
+            if (E3_PACE_SLEEP) __nanosleep(E3_PACE_SLEEP);
+        }
+    if (s + 1 < P.nstrips && b + 1 < (int)gridDim.x)
+        while (ld_relaxed(P.progress + b + 1) < target) {
+            if (E3_PACE_SLEEP) __nanosleep(E3_PACE_SLEEP);
+        }
+}
+__device__ __forceinline__ void pace_publish(const Params& P, int n) {
+    if (P.progress) st_relaxed(P.progress + vblock(P), P.epoch + (unsigned long long)n);
+}
 
 template <int FORM>
 __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned char* smem, uint64_t* bars,
@@ -200,6 +272,8 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
         }
         return;
     }
+    // The modal stiffness is symmetric: a mirrored entry reads its partner's
+    // operand (KH[1] for entry 9, ...), so one uniform-register load serves both.
     // modal coefficients C[s] (z butterflies), s = sx + 2 sy + 4 sz; the modal
     // stiffness decouples into blocks {1,2,4}, {3,5,6}, {7}, evaluated and consumed
     // one after the other to keep few values live.
@@ -212,12 +286,12 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     const double F10 = KH[0] * c10 + KH[1] * c21 + KH[2] * c42;
     const double F11 = KH[3] * c11 + KH[4] * c20;
     const double F12 = KH[5] * c12 + KH[6] * c40;
-    const double F20 = KH[7] * c11 + KH[8] * c20;
-    const double F21 = KH[9] * c10 + KH[10] * c21 + KH[11] * c42;
+    const double F20 = KH[4] * c11 + KH[8] * c20;
+    const double F21 = KH[1] * c10 + KH[10] * c21 + KH[11] * c42;
     const double F22 = KH[12] * c22 + KH[13] * c41;
-    const double F40 = KH[14] * c12 + KH[15] * c40;
-    const double F41 = KH[16] * c22 + KH[17] * c41;
-    const double F42 = KH[18] * c10 + KH[19] * c21 + KH[20] * c42;
+    const double F40 = KH[6] * c12 + KH[15] * c40;
+    const double F41 = KH[13] * c22 + KH[17] * c41;
+    const double F42 = KH[2] * c10 + KH[11] * c21 + KH[20] * c42;
     // pair (0, 4): mode 0 (rigid translation) carries no force; the carried top
     // of this pair is stored with the opposite sign
     double f0[3];
@@ -237,11 +311,11 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
     const double F31 = KH[23] * c31 + KH[24] * c52;
     const double F32 = KH[25] * c32 + KH[26] * c51 + KH[27] * c60;
     const double F50 = KH[28] * c50 + KH[29] * c61;
-    const double F51 = KH[30] * c32 + KH[31] * c51 + KH[32] * c60;
-    const double F52 = KH[33] * c31 + KH[34] * c52;
-    const double F60 = KH[35] * c32 + KH[36] * c51 + KH[37] * c60;
-    const double F61 = KH[38] * c50 + KH[39] * c61;
-    const double F62 = KH[40] * c30 + KH[41] * c62;
+    const double F51 = KH[26] * c32 + KH[31] * c51 + KH[32] * c60;
+    const double F52 = KH[24] * c31 + KH[34] * c52;
+    const double F60 = KH[27] * c32 + KH[32] * c51 + KH[37] * c60;
+    const double F61 = KH[29] * c50 + KH[39] * c61;
+    const double F62 = KH[22] * c30 + KH[41] * c62;
     // pairs (1, 5) and (2, 6)
     double f1[3], f2[3];
     {
@@ -370,7 +444,7 @@ static_assert(NWARP == 8, "warp roles assume 8 cell warps");
 template <class F>
 __device__ __forceinline__ void walk(const Params& P, F&& f) {
     const Geo& g = P.g;
-    for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
+    for (int item = vblock(P); item < P.nitems; item += gridDim.x) {
         const int s = item % P.nstrips;
         const int ka = g.kb + (item / P.nstrips) * P.chunk;
         const int kb = min(ka + P.chunk, g.ke);
@@ -387,7 +461,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
-    if (skip_step(P.status, P.step, P.nsteps)) return;
+    if (skip_step(P.status, P.step, P.nsteps)) {
+        if (threadIdx.x == 0) pace_publish(P, 1 << 30);
+        return;
+    }
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
@@ -401,13 +478,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         prefetch_tmap(&M.m);
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-        pc->item = blockIdx.x;
+        pc->item = vblock(P);
         pc->t = 0;
         pc->kk = 0;
+        pc->n = 0;
         pc->set(P);
         for (int s = 0; s < S - 1 && pc->valid; ++s) {
+            pace_wait(P, pc->n);
             issue<FORM>(P, *pc, smem, bars, s, M);
             pc->next(P);
+            pace_publish(P, pc->n);
         }
     }
     tmem_fence_before();
@@ -472,12 +552,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         walk(P, [&](bool, int, int, int, int, bool) {
             __syncthreads();  // cell warps done with task q, node warps with task q-1
             if (l == 0 && pc->valid) {  // refill the stage of task q-1
+                pace_wait(P, pc->n);
                 issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
                 pc->next(P);
+                pace_publish(P, pc->n);
             }
             if (++st == S) st = 0;
         });
         __syncthreads();
+        if (l == 0) pace_publish(P, 1 << 30);  // done: never hold the neighbours back
     } else {
         // ------------------------------------------------------------ node warps
         regs_shrink<REG_NODE>();
