@@ -63,20 +63,31 @@ int blocks_for(long long n, int threads = 256) { return (int)std::max(1LL, (n + 
 int upload(petto_ctx* ctx, double* dst, const double* host, int comps) {
     const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
-    for (int c = 0; c < comps; ++c)
-        CK(cudaMemcpy2DAsync(dst + c * g.Ns, (size_t)g.px * 8, host + c * N + (long long)g.ks0 * g.nx * g.ny,
-                             (size_t)g.nx * 8, (size_t)g.nx * 8, (size_t)g.ny * g.nzs, cudaMemcpyHostToDevice,
-                             ctx->stream));
+    for (int c = 0; c < comps; ++c) {
+        const double* src = host + c * N + (long long)g.ks0 * g.nx * g.ny;
+        if (g.px == g.nx)  // unpadded rows: one linear copy (full copy-engine rate)
+            CK(cudaMemcpyAsync(dst + c * g.Ns, src, sizeof(double) * (size_t)g.nx * g.ny * g.nzs,
+                               cudaMemcpyHostToDevice, ctx->stream));
+        else
+            CK(cudaMemcpy2DAsync(dst + c * g.Ns, (size_t)g.px * 8, src, (size_t)g.nx * 8, (size_t)g.nx * 8,
+                                 (size_t)g.ny * g.nzs, cudaMemcpyHostToDevice, ctx->stream));
+    }
     return PETTO_OK;
 }
 
 int download(petto_ctx* ctx, double* host, const double* src, int comps) {
     const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
-    for (int c = 0; c < comps; ++c)
-        CK(cudaMemcpy2DAsync(host + c * N + (long long)g.kb * g.nx * g.ny, (size_t)g.nx * 8,
-                             src + c * g.Ns + lidx(g, 0, 0, g.kb), (size_t)g.px * 8, (size_t)g.nx * 8,
-                             (size_t)g.ny * (g.ke - g.kb), cudaMemcpyDeviceToHost, ctx->stream));
+    for (int c = 0; c < comps; ++c) {
+        double* dst = host + c * N + (long long)g.kb * g.nx * g.ny;
+        const double* s = src + c * g.Ns + lidx(g, 0, 0, g.kb);
+        if (g.px == g.nx)
+            CK(cudaMemcpyAsync(dst, s, sizeof(double) * (size_t)g.nx * g.ny * (g.ke - g.kb), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+        else
+            CK(cudaMemcpy2DAsync(dst, (size_t)g.nx * 8, s, (size_t)g.px * 8, (size_t)g.nx * 8,
+                                 (size_t)g.ny * (g.ke - g.kb), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     return PETTO_OK;
 }
 
