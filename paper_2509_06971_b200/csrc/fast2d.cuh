@@ -5,6 +5,8 @@
 // sets are L2-resident, so these are latency/launch-bound rather than HBM-bound).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace petto_b200 {
@@ -23,6 +25,7 @@ struct FusedParams {
     double src_uniform;
     double kh[10];      // 2D modal stiffness
     double e_scale;     // sum of 4 corner E -> E_cell
+    double hih2[3];     // heat: 0.5 / h_a^2
     double inv_base;    // 1/(hx hy [hz])
     double* partials;   // per-block r^2 (nullable)
     DeviceStatus* status;
@@ -70,90 +73,149 @@ __device__ __forceinline__ void finish_block(const FusedParams& P, double rsq, u
     }
 }
 
+// Heat: one owned node t (HeatOperator::residual + the update).
+__device__ __forceinline__ void heat_node(const FusedParams& P, long long t, double& rsq, unsigned& bad) {
+    const Geo& g = P.g;
+    const long long plane = (long long)g.nx * g.ny;
+    const int k = g.kb + (int)(t / plane);
+    const long long rr = t - (long long)(k - g.kb) * plane;
+    const int j = (int)(rr / g.nx);
+    const int i = (int)(rr - (long long)j * g.nx);
+    const long long node = lidx(g, i, j, k);
+    const double* T = P.cur + node;
+    const double* kp = P.prop + node;
+    if (!(kp[0] > 0.0)) bad |= 2u;
+    double acc = flux_fast(T, kp, i, g.nx, 1, P.hih2[0]) + flux_fast(T, kp, j, g.ny, g.px, P.hih2[1]);
+    if (g.nz > 1) acc += flux_fast(T, kp, k, g.nz, (long long)g.px * g.ny, P.hih2[2]);
+    const double r = acc + (P.src ? P.src[node] : P.src_uniform);
+    const double nv = fused_update(P, r, T[0], node, 0, P.mask[node], rsq);
+    bad |= !isfinite(nv);
+    P.next[node] = nv;
+}
+
 // Heat: grid-stride over owned nodes (fixed grid => deterministic partials).
 __global__ void __launch_bounds__(256) k_heat_fast(const FusedParams P) {
     const Geo& g = P.g;
     if (skip_step(P.status, P.step, P.nsteps)) return;
-    const long long plane = (long long)g.nx * g.ny;
-    const long long owned = plane * (g.ke - g.kb);
-    double hih2[3];
-    for (int a = 0; a < 3; ++a) hih2[a] = 0.5 / (g.h[a] * g.h[a]);
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
     double rsq = 0.0;
     unsigned bad = 0;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int k = g.kb + (int)(t / plane);
-        const long long rr = t - (long long)(k - g.kb) * plane;
-        const int j = (int)(rr / g.nx);
-        const int i = (int)(rr - (long long)j * g.nx);
-        const long long node = lidx(g, i, j, k);
-        const double* T = P.cur + node;
-        const double* kp = P.prop + node;
-        if (!(kp[0] > 0.0)) bad |= 2u;
-        double acc = flux_fast(T, kp, i, g.nx, 1, hih2[0]) + flux_fast(T, kp, j, g.ny, g.px, hih2[1]);
-        if (g.nz > 1) acc += flux_fast(T, kp, k, g.nz, (long long)g.px * g.ny, hih2[2]);
-        const double r = acc + (P.src ? P.src[node] : P.src_uniform);
-        const double nv = fused_update(P, r, T[0], node, 0, P.mask[node], rsq);
-        bad |= !isfinite(nv);
-        P.next[node] = nv;
-    }
+         t += (long long)gridDim.x * blockDim.x)
+        heat_node(P, t, rsq, bad);
     finish_block<256>(P, rsq, bad);
 }
 
 // 2D plane-strain elasticity: each node gathers the corner forces of its (up to)
 // four cells, evaluated in the modal basis (stiffness.hpp pattern order).
+__device__ __forceinline__ void elastic2d_node(const FusedParams& P, long long t, double& rsq, unsigned& bad) {
+    const Geo& g = P.g;
+    const double* k = P.kh;
+    const int j = (int)(t / g.nx);
+    const int i = (int)(t - (long long)j * g.nx);
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {  // this node is corner m of cell (i - bx, j - by)
+        const int ci = i - (m & 1), cj = j - (m >> 1);
+        if (ci < 0 || ci > g.nx - 2 || cj < 0 || cj > g.ny - 2) continue;
+        const long long b = lidx(g, ci, cj, 0);
+        const long long o[4] = {b, b + 1, b + g.px, b + g.px + 1};
+        double C[4][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const double* u = P.cur + c * g.Ns;
+            const double v0 = u[o[0]], v1 = u[o[1]], v2 = u[o[2]], v3 = u[o[3]];
+            C[1][c] = (v0 - v1) + (v2 - v3);
+            C[2][c] = (v0 + v1) - (v2 + v3);
+            C[3][c] = (v0 - v1) - (v2 - v3);
+        }
+        const double ec = ((P.prop[o[0]] + P.prop[o[1]]) + (P.prop[o[2]] + P.prop[o[3]])) * P.e_scale;
+        const double F10 = ec * (k[0] * C[1][0] + k[1] * C[2][1]);
+        const double F11 = ec * (k[2] * C[1][1] + k[3] * C[2][0]);
+        const double F20 = ec * (k[4] * C[1][1] + k[5] * C[2][0]);
+        const double F21 = ec * (k[6] * C[1][0] + k[7] * C[2][1]);
+        const double F30 = ec * (k[8] * C[3][0]);
+        const double F31 = ec * (k[9] * C[3][1]);
+        const double s1 = (m & 1) ? -1.0 : 1.0, s2 = (m & 2) ? -1.0 : 1.0, s3 = s1 * s2;
+        acc[0] += s1 * F10 + s2 * F20 + s3 * F30;
+        acc[1] += s1 * F11 + s2 * F21 + s3 * F31;
+    }
+    const long long node = lidx(g, i, j, 0);
+    const double invv = inv_volume_fast(g, P.inv_base, i, j, 0);
+    const unsigned char mk = P.mask[node];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const long long e = c * g.Ns + node;
+        const double f = ((mk & 8) && !((mk >> c) & 1)) ? P.aux[e] : 0.0;
+        const double r = -acc[c] * invv - f;
+        const double nv = fused_update(P, r, P.cur[e], e, c, mk, rsq);
+        bad |= !isfinite(nv);
+        P.next[e] = nv;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_elastic2d_fast(const FusedParams P) {
     const Geo& g = P.g;
     if (skip_step(P.status, P.step, P.nsteps)) return;
     const long long owned = (long long)g.nx * g.ny;
-    const double* k = P.kh;
     double rsq = 0.0;
     unsigned bad = 0;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int j = (int)(t / g.nx);
-        const int i = (int)(t - (long long)j * g.nx);
-        double acc[2] = {0.0, 0.0};
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {  // this node is corner m of cell (i - bx, j - by)
-            const int ci = i - (m & 1), cj = j - (m >> 1);
-            if (ci < 0 || ci > g.nx - 2 || cj < 0 || cj > g.ny - 2) continue;
-            const long long b = lidx(g, ci, cj, 0);
-            const long long o[4] = {b, b + 1, b + g.px, b + g.px + 1};
-            double C[4][2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const double* u = P.cur + c * g.Ns;
-                const double v0 = u[o[0]], v1 = u[o[1]], v2 = u[o[2]], v3 = u[o[3]];
-                C[1][c] = (v0 - v1) + (v2 - v3);
-                C[2][c] = (v0 + v1) - (v2 + v3);
-                C[3][c] = (v0 - v1) - (v2 - v3);
-            }
-            const double ec = ((P.prop[o[0]] + P.prop[o[1]]) + (P.prop[o[2]] + P.prop[o[3]])) * P.e_scale;
-            const double F10 = ec * (k[0] * C[1][0] + k[1] * C[2][1]);
-            const double F11 = ec * (k[2] * C[1][1] + k[3] * C[2][0]);
-            const double F20 = ec * (k[4] * C[1][1] + k[5] * C[2][0]);
-            const double F21 = ec * (k[6] * C[1][0] + k[7] * C[2][1]);
-            const double F30 = ec * (k[8] * C[3][0]);
-            const double F31 = ec * (k[9] * C[3][1]);
-            const double s1 = (m & 1) ? -1.0 : 1.0, s2 = (m & 2) ? -1.0 : 1.0, s3 = s1 * s2;
-            acc[0] += s1 * F10 + s2 * F20 + s3 * F30;
-            acc[1] += s1 * F11 + s2 * F21 + s3 * F31;
-        }
-        const long long node = lidx(g, i, j, 0);
-        const double invv = inv_volume_fast(g, P.inv_base, i, j, 0);
-        const unsigned char mk = P.mask[node];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const long long e = c * g.Ns + node;
-            const double f = ((mk & 8) && !((mk >> c) & 1)) ? P.aux[e] : 0.0;
-            const double r = -acc[c] * invv - f;
-            const double nv = fused_update(P, r, P.cur[e], e, c, mk, rsq);
-            bad |= !isfinite(nv);
-            P.next[e] = nv;
-        }
-    }
+         t += (long long)gridDim.x * blockDim.x)
+        elastic2d_node(P, t, rsq, bad);
     finish_block<256>(P, rsq, bad);
+}
+
+// Whole hybrid_solve (state_solver.hpp:480-498) of a small grid in ONE cooperative
+// launch: the per-step kernels of C1-C3 last a few microseconds, so launch and
+// drain dominate; here the steps are separated by grid-wide barriers instead.
+// Buffers swap exactly as in the host loop (next := previous, then swap); the
+// check_finite cadence is kept through skip_step, read after each barrier.
+struct SolveParams {
+    FusedParams base;     // geometry, fields and constants (cur/prev/next per step)
+    double* st[2];        // history: current = st[c], previous = st[1 - c]
+    int c0;               // current buffer at step 1
+    long long n_apt, n_pt;
+    int form_apt;         // 0 explicit, 1 semi-implicit
+    double a, b, inv;     // APT coefficients
+    double dt_pt;         // PT step
+};
+
+template <int PHYS>  // 0 heat, 1 2D elasticity
+__global__ void __launch_bounds__(256) k_small_solve(const SolveParams S) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    FusedParams P = S.base;
+    const Geo& g = P.g;
+    const long long owned = (long long)g.nx * g.ny * (g.ke - g.kb);
+    const long long nsteps = S.n_apt + S.n_pt;
+    int c = S.c0;
+    for (long long step = 1; step <= nsteps; ++step) {
+        if (skip_step(P.status, step, nsteps)) break;  // same value in every CTA (read after the barrier)
+        const bool apt = step <= S.n_apt;
+        P.form = apt ? S.form_apt : 2;
+        P.a = S.a;
+        P.b = S.b;
+        P.inv = S.inv;
+        P.dt = S.dt_pt;
+        P.cur = S.st[c];
+        P.prev = S.st[1 - c];
+        P.next = S.st[1 - c];
+        P.step = step;
+        double rsq = 0.0;
+        unsigned bad = 0;
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < owned;
+             t += (long long)gridDim.x * blockDim.x) {
+            if (PHYS == 0) heat_node(P, t, rsq, bad);
+            else elastic2d_node(P, t, rsq, bad);
+        }
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        if (bad && (threadIdx.x & 31) == 0) {
+            if (bad & 2u) atomicOr(&P.status->flags, 2u);
+            if (bad & 1u) mark_bad(P.status, step);
+        }
+        c ^= 1;
+        grid.sync();
+    }
 }
 
 }  // namespace petto_b200

@@ -293,6 +293,37 @@ void timing_end(petto_ctx* ctx, cudaEvent_t* ev, const char* name, double bytes)
     ctx->kernel_name = name;
 }
 
+// Parameters of the small fused kernels (heat 2D/3D, 2D elasticity) for one step.
+FusedParams fused_params(const petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, double* partials,
+                         long long step, long long nsteps) {
+    const Geo& g = ctx->g;
+    FusedParams P{};
+    P.g = g;
+    P.form = k.form;
+    P.dt = k.dt;
+    P.a = k.a;
+    P.b = k.b;
+    P.inv = k.inv;
+    P.cur = ctx->st[cur];
+    P.prev = ctx->st[prev];
+    P.next = next;
+    P.prop = ctx->prop;
+    P.mask = ctx->mask;
+    P.aux = ctx->aux;
+    P.src = ctx->src_uniform ? nullptr : ctx->src;
+    P.src_uniform = ctx->src_value;
+    for (int i = 0; i < 10 && i < (int)ctx->kh.size(); ++i) P.kh[i] = ctx->kh[i];
+    const double nu = ctx->desc.poisson_ratio;
+    P.e_scale = (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 4.0);
+    P.inv_base = g.dim == 3 ? 1.0 / (g.h[0] * g.h[1] * g.h[2]) : 1.0 / (g.h[0] * g.h[1]);
+    for (int a = 0; a < 3; ++a) P.hih2[a] = 0.5 / (g.h[a] * g.h[a]);
+    P.partials = partials;
+    P.status = ctx->status;
+    P.step = step;
+    P.nsteps = nsteps;
+    return P;
+}
+
 // One fused (fast) or replica state step: reads st[cur] (and st[prev]), writes
 // `next` (a state buffer or the residual scratch for form 3).
 int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, long long step, long long nsteps,
@@ -386,29 +417,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             if (partials) ctx->npartials_used = grid;
             return PETTO_OK;
         }
-        FusedParams P{};
-        P.g = g;
-        P.form = k.form;
-        P.dt = k.dt;
-        P.a = k.a;
-        P.b = k.b;
-        P.inv = k.inv;
-        P.cur = ctx->st[cur];
-        P.prev = ctx->st[prev];
-        P.next = next;
-        P.prop = ctx->prop;
-        P.mask = ctx->mask;
-        P.aux = ctx->aux;
-        P.src = ctx->src_uniform ? nullptr : ctx->src;
-        P.src_uniform = ctx->src_value;
-        for (int i = 0; i < 10 && i < (int)ctx->kh.size(); ++i) P.kh[i] = ctx->kh[i];
-        const double nu = ctx->desc.poisson_ratio;
-        P.e_scale = (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 4.0);
-        P.inv_base = g.dim == 3 ? 1.0 / (g.h[0] * g.h[1] * g.h[2]) : 1.0 / (g.h[0] * g.h[1]);
-        P.partials = partials;
-        P.status = ctx->status;
-        P.step = step;
-        P.nsteps = nsteps;
+        FusedParams P = fused_params(ctx, k, cur, prev, next, partials, step, nsteps);
         const int grid = (int)std::min<long long>(ctx->npartials, blocks_for(owned));
         timing_begin(ctx, ev);
         if (ctx->desc.physics == 0) {
@@ -940,6 +949,44 @@ int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
     return PETTO_OK;
 }
 
+// Small grids of the heat / 2D-elasticity operators: the whole hybrid_solve runs
+// as one cooperative launch (k_small_solve) instead of one launch per step.
+bool small_solve_ok(const petto_ctx* ctx) {
+    const Geo& g = ctx->g;
+    const bool small_op = ctx->desc.physics == 0 || g.dim == 2;
+    return ctx->mode == PETTO_MODE_FAST && small_op && !ctx->nccl_comm && !ctx->nb_lo && !ctx->nb_hi &&
+           owned_nodes(ctx) <= (16LL << 20);
+}
+
+int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long long n_apt, long long n_pt) {
+    SolveParams S{};
+    S.base = fused_params(ctx, ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], nullptr, 0, n_apt + n_pt);
+    S.st[0] = ctx->st[ctx->cur];
+    S.st[1] = ctx->st[ctx->prev];
+    S.c0 = 0;
+    S.n_apt = n_apt;
+    S.n_pt = n_pt;
+    S.form_apt = ka.form;
+    S.a = ka.a;
+    S.b = ka.b;
+    S.inv = ka.inv;
+    S.dt_pt = kp.dt;
+    const bool heat = ctx->desc.physics == 0;
+    const void* fn = heat ? (const void*)k_small_solve<0> : (const void*)k_small_solve<1>;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+    const int grid = (int)std::min<long long>((long long)std::max(per_sm, 1) * ctx->nsm, blocks_for(owned_nodes(ctx)));
+    void* args[] = {&S};
+    cudaEvent_t ev[2];
+    timing_begin(ctx, ev);
+    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, ctx->stream));
+    const double bpn = heat ? 33.0 : 57.0;  // APT bytes per node
+    timing_end(ctx, ev, "k_small_solve", (double)owned_nodes(ctx) * bpn * (double)(n_apt + n_pt));
+    ctx->launches++;
+    CKL();
+    return PETTO_OK;
+}
+
 // PTParams::validate (state_solver.hpp:25-33)
 static int validate_params(petto_ctx* ctx, const petto_pt_params* p) {
     if (!(p->dt_pt > 0.0) && p->n_pt > 0) return fail(ctx, PETTO_INVALID, "pt params: dt_pt must be positive");
@@ -960,13 +1007,17 @@ int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* ab
     long long step = 0;
     const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
     const StepCoef kp = coef(2, p->dt_pt, p->theta);
-    for (long s = 0; s < p->n_apt; ++s) {
+    if (small_solve_ok(ctx)) {
+        if (int rc = small_solve(ctx, ka, kp, p->n_apt, p->n_pt)) return rc;
+        if (nsteps % 2) std::swap(ctx->cur, ctx->prev);  // the kernel swapped nsteps times
+    }
+    for (long s = 0; s < p->n_apt && !small_solve_ok(ctx); ++s) {
         // next := previous buffer, written in place; then swap (state_solver.hpp:421, 440)
         if (int rc = state_step(ctx, ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
         std::swap(ctx->cur, ctx->prev);
         if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
     }
-    for (long s = 0; s < p->n_pt; ++s) {
+    for (long s = 0; s < p->n_pt && !small_solve_ok(ctx); ++s) {
         if (int rc = state_step(ctx, kp, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
         std::swap(ctx->cur, ctx->prev);
         if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
