@@ -226,9 +226,21 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
 int petto_dev_comm_unique_id(void* id128);
 int petto_dev_comm_init(petto_ctx* ctx, const void* id128, int rank, int nranks);
 
+/* Peer halo (optional, after comm_init): each rank exports the IPC handles of
+ * its state buffers and step inbox (PETTO_PEER_BLOB_BYTES bytes), the caller
+ * all-gathers the blobs, and every rank imports its -1 / +1 neighbours' (NULL
+ * at a physical end).  From then on the fused 3D steps of hybrid_solve store
+ * their boundary planes straight into the neighbours' ghost planes over
+ * NVLink and order the steps with stream-ordered flags (no NCCL call and no
+ * SM time for the halo); set_state takes part in the same step protocol. */
+#define PETTO_PEER_BLOB_BYTES 512
+int petto_dev_peer_export(petto_ctx* ctx, void* blob);
+int petto_dev_peer_import(petto_ctx* ctx, const void* lo_blob, const void* hi_blob);
+
 /* Single process driving several contexts (several GPUs, or one GPU in tests):
- * link the contexts of consecutive slabs, then solve them in lock step with
- * stream-ordered peer copies of the ghost planes. */
+ * link the contexts of consecutive slabs, then solve them in lock step: fused 3D
+ * steps use the peer halo (direct pointers), the other kernels stream-ordered
+ * peer copies of the ghost planes. */
 int petto_dev_group_link(petto_ctx** ctxs, int n);
 int petto_dev_group_hybrid_solve(petto_ctx** ctxs, int n, const petto_pt_params* p, int64_t* abort_step);
 

@@ -13,6 +13,17 @@
 
 namespace petto_b200 {
 
+// A neighbouring slab as seen from this context (peer-halo mode): its state
+// buffers (same device, P2P-enabled device or IPC-mapped), its layout, and the
+// inbox slot of it that this context signals after each fused step.
+struct PeerSlab {
+    double* st[3] = {nullptr, nullptr, nullptr};
+    long long Ns = 0;
+    int ks0 = 0;
+    unsigned long long* flag = nullptr;
+    bool ipc = false;  // st / inbox opened with cudaIpcOpenMemHandle
+    unsigned long long* ipc_inbox = nullptr;
+};
 
 }  // namespace petto_b200
 
@@ -84,6 +95,14 @@ struct petto_ctx {
     double* pmax = nullptr;        // per-block maxima [blocks][8]
     unsigned long long* count = nullptr;
     double* dscal = nullptr;       // device scalars for the design kernels
+
+    // peer halo (fused 3D steps write their boundary planes straight into the
+    // neighbours' ghost planes; stream memory operations order the steps)
+    petto_b200::PeerSlab peer_lo, peer_hi;
+    bool peer_halo = false;
+    unsigned long long* inbox = nullptr;  // [2]: last step finished by the lo / hi neighbour
+    unsigned long long peer_seq = 0;      // fused steps signalled so far
+    bool peer_step = false;               // the current state_step stores into the peers
 
     // slab decomposition: NCCL ranks or a local group of contexts
     int rank = 0, nranks = 1;

@@ -52,7 +52,7 @@ namespace e3 {
 #define E3_PACE_SLEEP 0
 #endif
 #ifndef E3_SMID_MAP
-#define E3_SMID_MAP 1
+#define E3_SMID_MAP 0
 #endif
 #ifndef E3_EXPERIMENT
 #define E3_EXPERIMENT 0  // 1: no TMA traffic (compute only), 2: no cell math (traffic only)
@@ -95,6 +95,11 @@ struct Params {
     // update coefficients: APT u' = c1 u - c2 u_prev + c3 r; PT u' = u + dt r
     double c1, c2, c3, dt;
     double* next;      // output field (may alias the previous iterate)
+    // peer halo: the neighbours' buffers of this step's output, offset so that this
+    // slab's local node index addresses them (null: no neighbour / not in use)
+    double* peer_lo;
+    double* peer_hi;
+    long long peer_lo_Ns, peer_hi_Ns;
     const double* aux; // pinned values / loads (3 x Ns)
     double* partials;  // per-CTA sum of r^2 over unconstrained entries (nullable)
     DeviceStatus* status;
@@ -410,11 +415,22 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
     }
     // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
     unsigned ex = 0;
-    double* dst = P.next + T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
+    const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
+    double* dst = P.next + local;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
         dst[c * g.Ns] = nv[c];
+    }
+    // a boundary plane is also the neighbour's ghost plane: store it there directly
+    // (NVLink / same-device stores, overlapped with the rest of the step)
+    if (kc == g.kb && P.peer_lo) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P.peer_lo[c * P.peer_lo_Ns + local] = nv[c];
+    }
+    if (kc == g.ke - 1 && P.peer_hi) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P.peer_hi[c * P.peer_hi_Ns + local] = nv[c];
     }
     bad |= ex;
 }
@@ -606,6 +622,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             ++q;
             if (++st == S) st = 0;
         });
+        if (P.peer_lo || P.peer_hi) __threadfence_system();  // peer stores before the step's signal
         __syncthreads();
     }
 

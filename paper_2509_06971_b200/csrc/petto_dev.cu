@@ -124,6 +124,57 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// Stream memory operations (driver API): stream-ordered waits on / writes of
+// 64-bit flags, used by the peer halo to order neighbouring slabs' steps without
+// the host and without occupying SMs.
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+StreamValueFn driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<StreamValueFn>(p);
+    return nullptr;
+}
+
+int stream_wait_geq(petto_ctx* ctx, unsigned long long* addr, unsigned long long v) {
+    static StreamValueFn fn = driver_fn("cuStreamWaitValue64");
+    if (!fn) return fail(ctx, PETTO_ERROR, "cuStreamWaitValue64 unavailable");
+    if (fn(reinterpret_cast<CUstream>(ctx->stream), reinterpret_cast<CUdeviceptr>(addr), v, 0x0 /*GEQ*/) !=
+        CUDA_SUCCESS)
+        return fail(ctx, PETTO_ERROR, "cuStreamWaitValue64 failed");
+    return PETTO_OK;
+}
+
+int stream_write(petto_ctx* ctx, unsigned long long* addr, unsigned long long v) {
+    static StreamValueFn fn = driver_fn("cuStreamWriteValue64");
+    if (!fn) return fail(ctx, PETTO_ERROR, "cuStreamWriteValue64 unavailable");
+    if (fn(reinterpret_cast<CUstream>(ctx->stream), reinterpret_cast<CUdeviceptr>(addr), v, 0x0 /*DEFAULT*/) !=
+        CUDA_SUCCESS)
+        return fail(ctx, PETTO_ERROR, "cuStreamWriteValue64 failed");
+    return PETTO_OK;
+}
+
+// Peer halo, per fused step `seq`: wait until both neighbours finished step seq-1
+// (their stores into our ghost planes are complete, and they no longer read the
+// ghost planes of theirs that this step overwrites) ...
+int peer_wait(petto_ctx* ctx, unsigned long long seq) {
+    if (ctx->peer_lo.st[0])
+        if (int rc = stream_wait_geq(ctx, ctx->inbox + 0, seq - 1)) return rc;
+    if (ctx->peer_hi.st[0])
+        if (int rc = stream_wait_geq(ctx, ctx->inbox + 1, seq - 1)) return rc;
+    return PETTO_OK;
+}
+
+// ... and after the step's kernel tell them step `seq` is done.
+int peer_signal(petto_ctx* ctx, unsigned long long seq) {
+    if (ctx->peer_lo.flag)
+        if (int rc = stream_write(ctx, ctx->peer_lo.flag, seq)) return rc;
+    if (ctx->peer_hi.flag)
+        if (int rc = stream_write(ctx, ctx->peer_hi.flag, seq)) return rc;
+    return PETTO_OK;
+}
+
 // TMA descriptors of the fused 3D kernel (and its cell-modulus field).  No L2
 // sector promotion: the 34-column U boxes start 256 B-aligned and would drag a
 // second 256 B block each, and the 32-byte mask rows a full 256 B block
@@ -360,6 +411,21 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             }
             P.dt = k.dt;
             P.next = next;
+            if (ctx->peer_step) {
+                int ob = -1;
+                for (int b = 0; b < 3; ++b)
+                    if (next == ctx->st[b]) ob = b;
+                if (ob < 0) return fail(ctx, PETTO_ERROR, "peer halo: output is not a state buffer");
+                const long long plane = (long long)g.px * g.ny;
+                if (ctx->peer_lo.st[0]) {
+                    P.peer_lo = ctx->peer_lo.st[ob] + (long long)(g.ks0 - ctx->peer_lo.ks0) * plane;
+                    P.peer_lo_Ns = ctx->peer_lo.Ns;
+                }
+                if (ctx->peer_hi.st[0]) {
+                    P.peer_hi = ctx->peer_hi.st[ob] + (long long)(g.ks0 - ctx->peer_hi.ks0) * plane;
+                    P.peer_hi_Ns = ctx->peer_hi.Ns;
+                }
+            }
             P.aux = ctx->aux;
             P.partials = partials;
             P.status = ctx->status;
@@ -694,6 +760,12 @@ void petto_dev_destroy(petto_ctx* ctx) {
     cudaFree(ctx->prop);
     cudaFree(ctx->ecell);
     cudaFree(ctx->progress);
+    for (petto_b200::PeerSlab* ps : {&ctx->peer_lo, &ctx->peer_hi}) {
+        if (!ps->ipc) continue;
+        for (double* p : ps->st) cudaIpcCloseMemHandle(p);
+        cudaIpcCloseMemHandle(ps->ipc_inbox);
+    }
+    cudaFree(ctx->inbox);
     cudaFree(ctx->aux);
     cudaFree(ctx->mask);
     cudaFree(ctx->src);
@@ -910,8 +982,16 @@ int petto_dev_set_state(petto_ctx* ctx, const double* current, const double* pre
     CK(cudaSetDevice(ctx->device));
     ctx->cur = 0;
     ctx->prev = 1;
+    // peer halo: the upload (ghost planes included) is a step of the neighbour
+    // protocol -- it waits until the neighbours stopped storing into our ghosts and
+    // tells them when their next stores may land
+    const unsigned long long seq = ctx->peer_halo ? ++ctx->peer_seq : 0;
+    if (seq)
+        if (int rc = peer_wait(ctx, seq)) return rc;
     if (int rc = upload(ctx, ctx->st[0], current, ctx->comps)) return rc;
     if (int rc = upload(ctx, ctx->st[1], previous ? previous : current, ctx->comps)) return rc;
+    if (seq)
+        if (int rc = peer_signal(ctx, seq)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->state_set = true;
     return PETTO_OK;
@@ -947,6 +1027,40 @@ int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
         CK(cudaStreamSynchronize(ctx->stream));
     }
     return PETTO_OK;
+}
+
+// Inbox of the peer halo: two step counters written by the neighbours.
+int peer_prepare(petto_ctx* ctx) {
+    if (!ctx->inbox) {
+        CK(cudaMalloc(&ctx->inbox, 2 * sizeof(unsigned long long)));
+    }
+    CK(cudaMemset(ctx->inbox, 0, 2 * sizeof(unsigned long long)));
+    ctx->peer_seq = 0;
+    return PETTO_OK;
+}
+
+// One step of hybrid_solve: next := previous buffer, written in place; then swap
+// (state_solver.hpp:421, 440).  Slab ranks then refresh their ghost planes: with
+// the peer halo the fused kernel already stored its boundary planes into the
+// neighbours' ghosts and the step is ordered by stream flags; otherwise NCCL.
+bool use_peer(const petto_ctx* ctx) {
+    return ctx->peer_halo && ctx->mode == PETTO_MODE_FAST && ctx->g.dim == 3 && ctx->desc.physics == 1;
+}
+
+int hybrid_step(petto_ctx* ctx, const StepCoef& k, long long step, long long nsteps) {
+    const bool peer = use_peer(ctx);
+    unsigned long long seq = 0;
+    if (peer) {
+        seq = ++ctx->peer_seq;
+        if (int rc = peer_wait(ctx, seq)) return rc;
+        ctx->peer_step = true;
+    }
+    const int rc = state_step(ctx, k, ctx->cur, ctx->prev, ctx->st[ctx->prev], step, nsteps, false);
+    ctx->peer_step = false;
+    if (rc) return rc;
+    std::swap(ctx->cur, ctx->prev);
+    if (peer) return peer_signal(ctx, seq);
+    return halo(ctx, F_STATE, ctx->cur);
 }
 
 // Small grids of the heat / 2D-elasticity operators: the whole hybrid_solve runs
@@ -1011,17 +1125,10 @@ int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* ab
         if (int rc = small_solve(ctx, ka, kp, p->n_apt, p->n_pt)) return rc;
         if (nsteps % 2) std::swap(ctx->cur, ctx->prev);  // the kernel swapped nsteps times
     }
-    for (long s = 0; s < p->n_apt && !small_solve_ok(ctx); ++s) {
-        // next := previous buffer, written in place; then swap (state_solver.hpp:421, 440)
-        if (int rc = state_step(ctx, ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
-        std::swap(ctx->cur, ctx->prev);
-        if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
-    }
-    for (long s = 0; s < p->n_pt && !small_solve_ok(ctx); ++s) {
-        if (int rc = state_step(ctx, kp, ctx->cur, ctx->prev, ctx->st[ctx->prev], ++step, nsteps, false)) return rc;
-        std::swap(ctx->cur, ctx->prev);
-        if (int rc = halo(ctx, F_STATE, ctx->cur)) return rc;
-    }
+    for (long s = 0; s < p->n_apt && !small_solve_ok(ctx); ++s)
+        if (int rc = hybrid_step(ctx, ka, ++step, nsteps)) return rc;
+    for (long s = 0; s < p->n_pt && !small_solve_ok(ctx); ++s)
+        if (int rc = hybrid_step(ctx, kp, ++step, nsteps)) return rc;
     // every rank aborts at the same check_finite step
     if (int rc = allreduce(ctx, &ctx->status->first_bad, 1, ncclInt64, ncclMin)) return rc;
     if (int rc = read_status(ctx)) return rc;
@@ -1512,6 +1619,66 @@ int petto_dev_comm_init(petto_ctx* ctx, const void* id128, int rank, int nranks)
     return PETTO_OK;
 }
 
+namespace {
+struct PeerBlob {
+    uint32_t magic;
+    int32_t ks0, kb, ke;
+    int64_t Ns;
+    cudaIpcMemHandle_t st[3];
+    cudaIpcMemHandle_t inbox;
+};
+static_assert(sizeof(PeerBlob) <= PETTO_PEER_BLOB_BYTES, "peer blob size");
+constexpr uint32_t PEER_MAGIC = 0x50455452u;
+}  // namespace
+
+int petto_dev_peer_export(petto_ctx* ctx, void* blob) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = peer_prepare(ctx)) return rc;
+    PeerBlob b{};
+    b.magic = PEER_MAGIC;
+    b.ks0 = ctx->g.ks0;
+    b.kb = ctx->g.kb;
+    b.ke = ctx->g.ke;
+    b.Ns = ctx->g.Ns;
+    for (int i = 0; i < 3; ++i) CK(cudaIpcGetMemHandle(&b.st[i], ctx->st[i]));
+    CK(cudaIpcGetMemHandle(&b.inbox, ctx->inbox));
+    std::memset(blob, 0, PETTO_PEER_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+    return PETTO_OK;
+}
+
+int petto_dev_peer_import(petto_ctx* ctx, const void* lo_blob, const void* hi_blob) {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->inbox) return fail(ctx, PETTO_INVALID, "peer halo: call petto_dev_peer_export first");
+    auto open = [&](petto_b200::PeerSlab& ps, const void* raw, bool lo) -> int {
+        ps = petto_b200::PeerSlab{};
+        if (!raw) return PETTO_OK;
+        PeerBlob b;
+        std::memcpy(&b, raw, sizeof(b));
+        if (b.magic != PEER_MAGIC) return fail(ctx, PETTO_INVALID, "peer halo: not a peer blob");
+        if ((lo && b.ke != ctx->g.kb) || (!lo && b.kb != ctx->g.ke))
+            return fail(ctx, PETTO_INVALID, "peer halo: the neighbour's planes do not adjoin this slab");
+        for (int i = 0; i < 3; ++i) {
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, b.st[i], cudaIpcMemLazyEnablePeerAccess));
+            ps.st[i] = static_cast<double*>(p);
+        }
+        void* q = nullptr;
+        CK(cudaIpcOpenMemHandle(&q, b.inbox, cudaIpcMemLazyEnablePeerAccess));
+        ps.ipc = true;
+        ps.ipc_inbox = static_cast<unsigned long long*>(q);
+        ps.flag = ps.ipc_inbox + (lo ? 1 : 0);  // our slot in the neighbour's inbox
+        ps.Ns = b.Ns;
+        ps.ks0 = b.ks0;
+        return PETTO_OK;
+    };
+    if (int rc = open(ctx->peer_lo, lo_blob, true)) return rc;
+    if (int rc = open(ctx->peer_hi, hi_blob, false)) return rc;
+    ctx->peer_halo = lo_blob || hi_blob;
+    ctx->peer_seq = 0;
+    return PETTO_OK;
+}
+
 int petto_dev_group_link(petto_ctx** c, int n) {
     for (int i = 0; i < n; ++i) {
         petto_ctx* x = c[i];
@@ -1527,6 +1694,7 @@ int petto_dev_group_link(petto_ctx** c, int n) {
         if (!x->ev_pull) CK(cudaEventCreateWithFlags(&x->ev_pull, cudaEventDisableTiming));
         CK(cudaEventRecord(x->ev_step, x->stream));
         CK(cudaEventRecord(x->ev_pull, x->stream));
+        if (int rc = peer_prepare(x)) return rc;
         for (petto_ctx* nb : {x->nb_lo, x->nb_hi}) {
             if (!nb || nb->device == x->device) continue;
             int can = 0;
@@ -1538,11 +1706,34 @@ int petto_dev_group_link(petto_ctx** c, int n) {
             }
         }
     }
+    // peer halo between the group's slabs: direct pointers (same process)
+    for (int i = 0; i < n; ++i) {
+        petto_ctx* ctx = c[i];  // error sink of CK()
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaDeviceSynchronize());
+    }
+    for (int i = 0; i < n; ++i) {
+        petto_ctx* x = c[i];
+        auto fill = [&](petto_b200::PeerSlab& ps, petto_ctx* nb, int slot) {
+            ps = petto_b200::PeerSlab{};
+            if (!nb) return;
+            for (int b = 0; b < 3; ++b) ps.st[b] = nb->st[b];
+            ps.Ns = nb->g.Ns;
+            ps.ks0 = nb->g.ks0;
+            ps.flag = nb->inbox + slot;
+        };
+        fill(x->peer_lo, x->nb_lo, 1);  // we are the lo neighbour's hi neighbour
+        fill(x->peer_hi, x->nb_hi, 0);
+        x->peer_halo = n > 1;
+        x->peer_seq = 0;
+    }
     return PETTO_OK;
 }
 
-// hybrid_solve over a linked group: every step runs on all slabs, then each slab
-// pulls its ghost planes from its neighbours (stream-ordered, no host sync).
+// hybrid_solve over a linked group: every step runs on all slabs.  Fused 3D steps
+// use the peer halo (boundary planes stored into the neighbours' ghosts, steps
+// ordered by stream flags); the other kernels pull the ghost planes afterwards
+// (stream-ordered copies, no host sync).
 int petto_dev_group_hybrid_solve(petto_ctx** c, int n, const petto_pt_params* p, int64_t* abort_step) {
     petto_ctx* ctx = c[0];  // error sink of CK()
     for (int i = 0; i < n; ++i) {
@@ -1559,6 +1750,13 @@ int petto_dev_group_hybrid_solve(petto_ctx** c, int n, const petto_pt_params* p,
     const StepCoef kp = coef(2, p->dt_pt, p->theta);
     for (long long step = 1; step <= nsteps; ++step) {
         const StepCoef& k = step <= p->n_apt ? ka : kp;
+        if (use_peer(c[0])) {
+            for (int i = 0; i < n; ++i) {
+                CK(cudaSetDevice(c[i]->device));
+                if (int rc = hybrid_step(c[i], k, step, nsteps)) return rc;
+            }
+            continue;
+        }
         for (int i = 0; i < n; ++i) {
             petto_ctx* x = c[i];
             CK(cudaSetDevice(x->device));

@@ -137,7 +137,7 @@ EXPORTED = [
     "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
     "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
     "petto_dev_kernel_timing", "petto_dev_kernel_stats", "petto_dev_comm_unique_id", "petto_dev_comm_init",
-    "petto_dev_group_link", "petto_dev_group_hybrid_solve",
+    "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_peer_export", "petto_dev_peer_import",
 ]
 
 
@@ -364,6 +364,20 @@ class Context:
         """Join the NCCL communicator of the slab decomposition (one GPU per rank)."""
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
         self._check(lib().petto_dev_comm_init(self.h, buf, int(rank), int(nranks)))
+
+    PEER_BLOB_BYTES = 512
+
+    def peer_export(self):
+        """IPC handles of this slab's state buffers and step inbox (peer halo)."""
+        buf = (C.c_ubyte * self.PEER_BLOB_BYTES)()
+        self._check(lib().petto_dev_peer_export(self.h, buf))
+        return bytes(buf)
+
+    def peer_import(self, lo=None, hi=None):
+        """Map the -1 / +1 neighbours' blobs (None at a physical end)."""
+        lb = (C.c_ubyte * self.PEER_BLOB_BYTES).from_buffer_copy(lo) if lo else None
+        hb = (C.c_ubyte * self.PEER_BLOB_BYTES).from_buffer_copy(hi) if hi else None
+        self._check(lib().petto_dev_peer_import(self.h, lb, hb))
 
     # -- instrumentation -------------------------------------------------------
     def stream(self):

@@ -117,3 +117,43 @@ def test_group_c4_size_fast():
     for c in ctxs:
         c.get_state(got, np.zeros(3 * g.num_nodes))
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_group_repeated_solves_with_new_states(nranks):
+    """Peer halo across solves: the state upload between two group solves is a
+    step of the neighbour protocol (no stale or overwritten ghost planes)."""
+    g = P.Grid.make3d(36, 16, 13, 2.0, 1.0, 0.7)
+    comps, prop, src, bc, cur, prev = inputs(g, 1)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=17, n_pt=4, form=1)
+    e, v = P.make_constraints(g, bc, comps)
+    cur2 = H.random_field(comps * g.num_nodes, 11, -0.02, 0.02)
+
+    def setup(ctx):
+        ctx.set_constraints(e, v)
+        ctx.set_source(src)
+        ctx.set_property(prop)
+        ctx.init_operator()
+        ctx.set_state(cur, prev)
+
+    one = D.Context(g, 1, 0.3)
+    setup(one)
+    one.hybrid_solve(p)
+    one.set_state(cur2, cur)
+    one.hybrid_solve(p)
+    want_c, want_p = one.get_state()
+
+    ctxs = [D.Context(g, 1, 0.3, k_range=slab.slab_range(r, nranks, g.n[2])) for r in range(nranks)]
+    for c in ctxs:
+        setup(c)
+    D.group_link(ctxs)
+    D.group_hybrid_solve(ctxs, p)
+    for c in ctxs:
+        c.set_state(cur2, cur)
+    D.group_hybrid_solve(ctxs, p)
+    got_c = np.full(comps * g.num_nodes, np.nan)
+    got_p = np.full(comps * g.num_nodes, np.nan)
+    for c in ctxs:
+        c.get_state(got_c, got_p)
+    assert np.array_equal(got_c, want_c) and np.array_equal(got_p, want_p)
