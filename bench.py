@@ -104,6 +104,7 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.skip = 0
 
     def __enter__(self):
         try:
@@ -112,6 +113,12 @@ class ClockSampler:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a moment to start: let its first sample arrive so the
+            # timed region is covered, then drop that pre-region sample
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.skip = len(self.lines)
         except OSError:
             self.proc = None
         return self
@@ -122,6 +129,10 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # a short timed region may end between two samples: wait for one more
+            n, t0 = len(self.lines), time.perf_counter()
+            while len(self.lines) == n and time.perf_counter() - t0 < 0.5 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -131,7 +142,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.skip:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue

@@ -75,8 +75,6 @@ struct petto_ctx {
     double ecell_scale = 0.0;
     CUtensorMap tU[3], tP[3], tC, tM;
     bool tmaps = false;
-    unsigned long long* progress = nullptr;  // strip pacing counters (one per SM)
-    unsigned long long launch_seq = 0;
 
     // design subsystem
     petto_material mat{};

@@ -45,15 +45,6 @@ namespace e3 {
 #ifndef E3_S
 #define E3_S 4
 #endif
-#ifndef E3_PACE
-#define E3_PACE 0  // strip pacing slack in tasks (0: off)
-#endif
-#ifndef E3_PACE_SLEEP
-#define E3_PACE_SLEEP 0
-#endif
-#ifndef E3_SMID_MAP
-#define E3_SMID_MAP 0
-#endif
 #ifndef E3_EXPERIMENT
 #define E3_EXPERIMENT 0  // 1: no TMA traffic (compute only), 2: no cell math (traffic only)
 #endif
@@ -108,27 +99,8 @@ struct Params {
     int nstrips;       // y strips of W rows
     int chunk;         // owned planes per z chunk (<= LMAX)
     int nitems;        // nstrips * chunks
-    // pacing of neighbouring strips (null: off): CTA b publishes the number of
-    // task loads it has issued in progress[b] (offset by epoch) and issues task x
-    // only once the CTAs of the strips above and below have issued task x - pace,
-    // so a halo row is read twice within a few tasks and the second read hits L2
-    unsigned long long* progress;
-    unsigned long long epoch;
-    int pace;
-    int smid_map;      // work items by SM id (see vblock)
 };
-#ifndef E3_CONST_KH
-#define E3_CONST_KH 0
-#endif
-
-// modal stiffness operands: kernel parameters, or (E3_CONST_KH) a __constant__
-// bank refreshed on the launching stream before each launch
-__constant__ double c_kh[48];
-#if E3_CONST_KH
-#define KH c_kh
-#else
 #define KH P.kh
-#endif
 
 // The tensor maps of one launch (kernel parameters, 64-byte aligned).
 struct Maps {
@@ -142,7 +114,7 @@ struct Maps {
 // tasks kk = 0 (prologue: node planes ka-1, ka) and kk >= 1 (owned planes
 // kc = ka + ZP (kk-1) ..., loading node planes kc+1 .. kc+ZP).
 struct Cursor {
-    int item, t, kk, s, ka, ntask, n;
+    int item, t, kk, s, ka, ntask;
     bool valid;
     __device__ void set(const Params& P) {
         valid = item < P.nitems;
@@ -152,7 +124,6 @@ struct Cursor {
         ntask = 1 + (min(P.chunk, P.g.ke - ka) + ZP - 1) / ZP;
     }
     __device__ void next(const Params& P) {
-        ++n;
         if (++kk == ntask) {
             kk = 0;
             if (++t == P.ntx) {
@@ -163,49 +134,6 @@ struct Cursor {
         }
     }
 };
-
-// Work-item index of this CTA.  With one item per SM (a cooperative launch of
-// exactly one CTA per SM) items follow the SM id, so consecutive strips -- which
-// read each other's halo rows -- run on neighbouring SMs of one die and share its
-// L2; otherwise the block index.
-__device__ __forceinline__ int vblock(const Params& P) {
-    if (P.smid_map) {
-        unsigned s;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
-        return (int)s;
-    }
-    return blockIdx.x;
-}
-
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Producer side of the strip pacing: wait until the neighbouring strips' CTAs
-// have issued task n - pace (one item per CTA; neighbours share the z chunk).
-// Relaxed accesses: the counters only pace the loads, they publish no data (a
-// release store would also wait for this thread's in-flight TMA loads).
-__device__ __forceinline__ void pace_wait(const Params& P, int n) {
-    if (!P.progress || n < P.pace) return;
-    const unsigned long long target = P.epoch + (unsigned long long)(n - P.pace);
-    const int b = vblock(P), s = b % P.nstrips;
-    if (s > 0)
-        while (ld_relaxed(P.progress + b - 1) < target) {
-            if (E3_PACE_SLEEP) __nanosleep(E3_PACE_SLEEP);
-        }
-    if (s + 1 < P.nstrips && b + 1 < (int)gridDim.x)
-        while (ld_relaxed(P.progress + b + 1) < target) {
-            if (E3_PACE_SLEEP) __nanosleep(E3_PACE_SLEEP);
-        }
-}
-__device__ __forceinline__ void pace_publish(const Params& P, int n) {
-    if (P.progress) st_relaxed(P.progress + vblock(P), P.epoch + (unsigned long long)n);
-}
 
 template <int FORM>
 __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned char* smem, uint64_t* bars,
@@ -460,7 +388,7 @@ static_assert(NWARP == 8, "warp roles assume 8 cell warps");
 template <class F>
 __device__ __forceinline__ void walk(const Params& P, F&& f) {
     const Geo& g = P.g;
-    for (int item = vblock(P); item < P.nitems; item += gridDim.x) {
+    for (int item = blockIdx.x; item < P.nitems; item += gridDim.x) {
         const int s = item % P.nstrips;
         const int ka = g.kb + (item / P.nstrips) * P.chunk;
         const int kb = min(ka + P.chunk, g.ke);
@@ -477,10 +405,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
-    if (skip_step(P.status, P.step, P.nsteps)) {
-        if (threadIdx.x == 0) pace_publish(P, 1 << 30);
-        return;
-    }
+    if (skip_step(P.status, P.step, P.nsteps)) return;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
@@ -494,16 +419,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         prefetch_tmap(&M.m);
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-        pc->item = vblock(P);
+        pc->item = blockIdx.x;
         pc->t = 0;
         pc->kk = 0;
-        pc->n = 0;
         pc->set(P);
         for (int s = 0; s < S - 1 && pc->valid; ++s) {
-            pace_wait(P, pc->n);
             issue<FORM>(P, *pc, smem, bars, s, M);
             pc->next(P);
-            pace_publish(P, pc->n);
         }
     }
     tmem_fence_before();
@@ -568,15 +490,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         walk(P, [&](bool, int, int, int, int, bool) {
             __syncthreads();  // cell warps done with task q, node warps with task q-1
             if (l == 0 && pc->valid) {  // refill the stage of task q-1
-                pace_wait(P, pc->n);
                 issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
                 pc->next(P);
-                pace_publish(P, pc->n);
             }
             if (++st == S) st = 0;
         });
         __syncthreads();
-        if (l == 0) pace_publish(P, 1 << 30);  // done: never hold the neighbours back
     } else {
         // ------------------------------------------------------------ node warps
         regs_shrink<REG_NODE>();

@@ -185,11 +185,6 @@ int make_tmaps(petto_ctx* ctx) {
     if (!enc) return fail(ctx, PETTO_ERROR, "cuTensorMapEncodeTiled unavailable");
     if (!ctx->ecell && cudaMalloc(&ctx->ecell, (size_t)g.Ns * sizeof(double)) != cudaSuccess)
         return fail(ctx, PETTO_ERROR, "out of device memory (cell modulus)");
-    if (!ctx->progress) {
-        if (cudaMalloc(&ctx->progress, sizeof(unsigned long long) * ctx->nsm) != cudaSuccess)
-            return fail(ctx, PETTO_ERROR, "out of device memory (pacing counters)");
-        cudaMemsetAsync(ctx->progress, 0, sizeof(unsigned long long) * ctx->nsm, ctx->stream);
-    }
     const cuuint64_t d4[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs, 3};
     const cuuint64_t s4[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8, (cuuint64_t)g.Ns * 8};
     const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, e3::ZP, 3};
@@ -447,27 +442,11 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             M.c = ctx->tC;
             M.p = ctx->tP[prev];
             M.m = ctx->tM;
-            // strip pacing and SM-id work items (one item per CTA only) rely on every
-            // CTA being resident, so those launches are cooperative (or fail)
-            const bool paced = E3_PACE > 0 && P.nitems <= grid;
-            P.progress = paced ? ctx->progress : nullptr;
-            P.epoch = (++ctx->launch_seq) << 32;
-            P.pace = E3_PACE;
-            P.smid_map = E3_SMID_MAP && grid == ctx->nsm && P.nitems == grid;
-            const bool coop = paced || P.smid_map;
-#if E3_CONST_KH
-            CK(cudaMemcpyToSymbolAsync(e3::c_kh, P.kh, sizeof(double) * 45, 0, cudaMemcpyHostToDevice, ctx->stream));
-#endif
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
             cfg.blockDim = dim3(e3::WS_THREADS);
             cfg.dynamicSmemBytes = e3::SMEM_BYTES;
             cfg.stream = ctx->stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeCooperative;
-            attr[0].val.cooperative = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = coop ? 1 : 0;
             timing_begin(ctx, ev);
             cudaError_t le;
             switch (k.form) {
@@ -759,7 +738,6 @@ void petto_dev_destroy(petto_ctx* ctx) {
     for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
     cudaFree(ctx->prop);
     cudaFree(ctx->ecell);
-    cudaFree(ctx->progress);
     for (petto_b200::PeerSlab* ps : {&ctx->peer_lo, &ctx->peer_hi}) {
         if (!ps->ipc) continue;
         for (double* p : ps->st) cudaIpcCloseMemHandle(p);
