@@ -304,13 +304,25 @@ StepCoef coef(int form, double dt, double theta) {
 // Work plan of the fused 3D kernel: items = strips x z-chunks, one CTA per SM.
 // Chunks are as few as fill the SMs (each chunk restarts the z stream: two extra
 // planes), at least 8 planes long, at most LMAX.
-void plan_3d(const petto_ctx* ctx, int nstrips, int& chunks, int& grid) {
+void plan_3d(const petto_ctx* ctx, int nstrips, int& chunk, int& nitems, int& grid) {
+    // Work items = y-strips x z-chunks of an even length L <= LMAX, one CTA per SM.
+    // A CTA's time is (items per CTA) x (x tiles) x (a prologue, ~0.6 of a two-plane
+    // task, + L/2 tasks): pick the L that minimises it (a partial second wave costs
+    // a whole wave; shorter chunks restart the z stream more often).
     const int nzo = ctx->g.ke - ctx->g.kb;
-    // a single wave: strips x chunks <= SMs (a partial second wave would double the time)
-    chunks = std::max(1, ctx->nsm / nstrips);
-    chunks = std::min(chunks, std::max(1, nzo / 8));
-    chunks = std::max(chunks, (nzo + e3::LMAX - 1) / e3::LMAX);
-    grid = std::min(ctx->nsm, nstrips * chunks);
+    double best = 1e300;
+    chunk = 2;
+    for (int L = 2; L <= std::max(2, std::min(e3::LMAX, nzo + (nzo & 1))); L += 2) {
+        const int items = nstrips * ((nzo + L - 1) / L);
+        const int waves = (items + ctx->nsm - 1) / ctx->nsm;
+        const double t = waves * (0.6 + 0.5 * L);
+        if (t < best - 1e-9) {
+            best = t;
+            chunk = L;
+        }
+    }
+    nitems = nstrips * ((nzo + chunk - 1) / chunk);
+    grid = std::min(ctx->nsm, nitems);
 }
 
 void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
@@ -428,14 +440,8 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             P.nsteps = nsteps;
             P.ntx = (g.nx + 31) / 32;
             P.nstrips = (g.ny + e3::W - 1) / e3::W;
-            int chunks = 0, grid = 0;
-            plan_3d(ctx, P.nstrips, chunks, grid);
-            const int nzo = g.ke - g.kb;
-            P.chunk = (nzo + chunks - 1) / chunks;
-            P.chunk += P.chunk & 1;  // even chunks: whole two-plane tasks
-            P.chunk = std::min(P.chunk, e3::LMAX);
-            P.nitems = P.nstrips * ((nzo + P.chunk - 1) / P.chunk);
-            grid = std::min(grid, P.nitems);
+            int grid = 0;
+            plan_3d(ctx, P.nstrips, P.chunk, P.nitems, grid);
             if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
             e3::Maps M;
             M.u = ctx->tU[cur];
