@@ -503,13 +503,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         double ucar[3] = {0.0, 0.0, 0.0};
         uint32_t st = 0, q = 0;
         const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
+        Tile T{};  // set at each x tile's prologue task
         walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
             __syncthreads();  // the cell warps finished task q
             tmem_fence_after();
             const unsigned char* sb = smem + st * STAGE_BYTES;
             const double* su = reinterpret_cast<const double*>(sb + OFF_U) + v * BOXX + l;  // plane 0, row v
-            if (own) {
-                Tile T;
+            if (!own) {
                 T.t = t;
                 const int i = t * 32 + l, j = s * W - 1 + v;
                 T.upd = i < g.nx && j < g.ny;
@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 T.node0 = (long long)j * g.px + i;
                 T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + v * 3;
                 T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + v * 3;
+            } else {
                 double Yv[12];
                 tmem_ld12(tq + (q & 1) * 32, Yv);
                 const double Y0[2][3] = {{Yv[0], Yv[1], Yv[2]}, {Yv[3], Yv[4], Yv[5]}};
