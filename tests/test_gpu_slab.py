@@ -157,3 +157,23 @@ def test_group_repeated_solves_with_new_states(nranks):
     for c in ctxs:
         c.get_state(got_c, got_p)
     assert np.array_equal(got_c, want_c) and np.array_equal(got_p, want_p)
+
+
+@pytest.mark.parametrize("nproc", [2, 3])
+def test_peer_halo_multiprocess(nproc):
+    """Peer halo across processes (CUDA IPC + cross-process stream flags): ranks
+    share the one GPU; only streams wait on flags, no kernel waits on a rank."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.join(root, "tools", "mp_peer_check.py"), "--device", "0"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"peer halo, {nproc} processes: bit-identical" in r.stdout
