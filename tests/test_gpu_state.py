@@ -254,3 +254,25 @@ def test_iterate_to_tolerance_elastic_mms_fast(port):
     got = D.iterate_to_tolerance(hist, op, 1, p, 1e-3, 3000)
     assert got.converged == want.converged
     assert abs(got.iterations - want.iterations) <= 1
+
+
+@pytest.mark.parametrize("n_apt", [150, 230])
+def test_elasticity3d_reckless_abort_step(n_apt):
+    """check_finite cadence on the fused 3D path: a blowing-up APT solve aborts at
+    the same check (a multiple of 100, or the last step) in FAST and REPLICA mode
+    (kernels after the first non-finite step's check are skipped)."""
+    g = P.Grid.make3d(40, 17, 12, 2.0, 1.0, 0.7)
+    E = H.random_modulus(g, 2)
+    f = H.sparse_loads(g, 3, 3)
+    bc = H.elastic_bc(g, "x_hi")
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=40.0 * h, theta=1.0, n_apt=n_apt, n_pt=0, form=0)
+    steps = []
+    for mode in (REPLICA, FAST):
+        op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=mode)
+        hist = D.StateHistory.of(H.random_field(3 * g.num_nodes, 9, -1e-3, 1e-3))
+        with pytest.raises(D.NumericalAbort) as ei:
+            D.hybrid_solve(hist, op, p)
+        steps.append(ei.value.step)
+    assert steps[0] == steps[1]
+    assert steps[0] % 100 == 0 or steps[0] == n_apt
