@@ -13,18 +13,21 @@
 //   * the cell modulus E_cell (the corner tree sum times the operator scale,
 //     state_solver.hpp:336-343) is a per-cell field computed once per property
 //     change (k_cell_modulus), so a cell costs one load instead of eight;
-//   * CTA = 8 warps: lane l <-> x = i0 + l (32 nodes), warp w <-> row j0-1+w
-//     (warp 0 is the y-halo row of cells whose top corners feed row j0);
-//   * each CTA streams along z (the outermost axis), ZP node planes per task: per
-//     cell plane it keeps the previous plane's y/x-butterflies (12 doubles) and
-//     the top-face contributions (12 doubles) in registers;
+//   * a tile = 32 x-columns (lane l <-> x = i0 + l) by 8 rows j0-1 .. j0+6 (row
+//     j0-1 is the y-halo row of cells whose top corners feed row j0); the CTA is
+//     warp-specialised (16 warps, see k_elastic3d_fast): 8 cell warps, one per
+//     row, stream the z axis (the outermost), ZP node planes per task, keeping
+//     the previous plane's y/x-butterflies (12 doubles) and the top-face sums
+//     (12 doubles) in registers; 7 node warps assemble and update the owned rows
+//     one task behind; one producer warp;
 //   * node planes arrive by TMA (cp.async.bulk.tensor, zero-filled outside the
 //     grid) into an S-stage shared-memory ring guarded by mbarriers, issued S-1
-//     tasks ahead by one elected thread;
-//   * x-neighbour contributions travel by warp shuffle, y-neighbour ones through
-//     a double-buffered shared tile (one CTA barrier per task, i.e. per ZP
-//     planes), and the previous x-tile's last column through a small shared
-//     "x-halo" array -- a CTA walks the x-tiles of its (strip, z-chunk) item
+//     tasks ahead by the producer;
+//   * x-neighbour contributions travel by warp shuffle, a row's face sums to its
+//     node warp through tensor memory, the row-(j+1) shares through a
+//     double-buffered shared tile (one CTA barrier per task, i.e. per ZP planes),
+//     and the previous x-tile's last column through a small shared "x-halo"
+//     array -- a CTA walks the x-tiles of its (strip, z-chunk) item
 //     sequentially, so no cell is computed twice in x;
 //   * work item = (y-strip, z-chunk); item b -> CTA b with strips fastest, so the
 //     CTAs sharing a strip boundary stream the same planes at the same time and
@@ -49,7 +52,7 @@ namespace e3 {
 #define E3_EXPERIMENT 0  // 1: no TMA traffic (compute only), 2: no cell math (traffic only)
 #endif
 constexpr int W = E3_W;        // owned node rows per tile
-constexpr int NWARP = W + 1;   // + y-halo warp
+constexpr int NWARP = W + 1;   // cell rows per tile (+ y-halo row)
 constexpr int NTHREADS = NWARP * 32;
 constexpr int ZP = 2;          // node planes per task
 constexpr int BOXX = 34;       // TMA box width of U (33 columns used; 16-byte multiple)
