@@ -200,7 +200,8 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": g.num_nodes / (v * 1e9) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem)",
-        "config": {"workload": f"{a.config}: {cfg.nx}x{cfg.ny}x{cfg.nz} cantilever3d elasticity, APT steps",
+        "config": {"workload": f"{a.config}: {cfg.nx}x{cfg.ny}x{cfg.nz} {cfg.preset} "
+                               f"{'heat' if prob.physics == 0 else 'elasticity'}, APT steps",
                    "sample": "1 APT step per bench step"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
                          "sample": "1 APT step of the full grid per bench step"},
@@ -359,7 +360,8 @@ def run_ours(a):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem: initial design, zero state)",
-        "config": {"workload": f"{a.config}: {g.n[0]}x{g.n[1]}x{g.n[2]} cantilever3d elasticity "
+        "config": {"workload": f"{a.config}: {g.n[0]}x{g.n[1]}x{g.n[2]} {cfg.preset} "
+                               f"{'heat' if prob.physics == 0 else 'elasticity'} "
                                f"({N} nodes), hybrid_solve with n_apt={a.n_apt}, n_pt=0, "
                                f"form={'semi_implicit' if sched.pt.form else 'explicit'}",
                    "l2": "inputs larger than L2 (state 2x805 MB + modulus 268 MB per step)",
