@@ -199,7 +199,7 @@ def run_reference(a):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": g.num_nodes / (v * 1e9) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (reference {a.config} problem)",
         "config": {"workload": f"{a.config}: {cfg.nx}x{cfg.ny}x{cfg.nz} {cfg.preset} "
                                f"{'heat' if prob.physics == 0 else 'elasticity'}, APT steps",
                    "sample": "1 APT step per bench step"},
@@ -359,7 +359,7 @@ def run_ours(a):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference C5 problem: initial design, zero state)",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (reference {a.config} problem: initial design, zero state)",
         "config": {"workload": f"{a.config}: {g.n[0]}x{g.n[1]}x{g.n[2]} {cfg.preset} "
                                f"{'heat' if prob.physics == 0 else 'elasticity'} "
                                f"({N} nodes), hybrid_solve with n_apt={a.n_apt}, n_pt=0, "
