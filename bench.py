@@ -246,10 +246,22 @@ def run_ours(a):
         ctx.comm_init(bytes(t.cpu().tolist()), rank, world)
         if a.halo == "peer":
             # peer halo: map the neighbours' state buffers (CUDA IPC over NVLink); the
-            # fused steps then store their boundary planes into the neighbours' ghosts
+            # fused steps then store their boundary planes into the neighbours' ghosts.
+            # Every rank must agree; if any rank cannot map its neighbours, all stay on NCCL.
             blobs = [None] * world
             torch.distributed.all_gather_object(blobs, ctx.peer_export())
-            ctx.peer_import(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank + 1 < world else None)
+            ok = True
+            try:
+                ctx.peer_import(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank + 1 < world else None)
+            except RuntimeError as ex:
+                print(f"rank {rank}: peer halo unavailable ({ex}); NCCL halo", file=sys.stderr)
+                ok = False
+            flags = [None] * world
+            torch.distributed.all_gather_object(flags, ok)
+            if not all(flags):
+                a.halo = "nccl"
+                if ok:
+                    ctx.peer_import(None, None)  # back to the NCCL halo
             torch.distributed.barrier()
     params = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, a.n_apt, 0, sched.pt.form)
 
