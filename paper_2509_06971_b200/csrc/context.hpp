@@ -73,7 +73,7 @@ struct petto_ctx {
     double* ecell = nullptr;
     bool ecell_valid = false;
     double ecell_scale = 0.0;
-    CUtensorMap tU[3], tP[3], tC, tM;
+    CUtensorMap tU[3], tP[3], tC, tM, tO[4];  // tO: st[0..2] and the residual scratch, box [3][1][W][32]
     bool tmaps = false;
 
     // design subsystem

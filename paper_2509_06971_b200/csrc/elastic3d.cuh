@@ -76,7 +76,9 @@ constexpr int YS = ZP * 6 * 32;             // one warp's y shares of one task
 
 constexpr int OFF_Y = S * STAGE_BYTES;                      // [2][NWARP][ZP][6][32] f64
 constexpr int OFF_X = OFF_Y + 2 * NWARP * YS * 8;           // [2][LMAX][NWARP][3] f64
-constexpr int OFF_BAR = OFF_X + 2 * LMAX * NWARP * 3 * 8;   // [S] full
+constexpr int OSTRIDE = 3 * W * 32;                         // one node plane of the output staging
+constexpr int OFF_O = OFF_X + 2 * LMAX * NWARP * 3 * 8;     // [2][ZP][3][W][32] f64 output staging
+constexpr int OFF_BAR = OFF_O + 2 * ZP * OSTRIDE * 8;       // [S] full
 constexpr int OFF_RED = OFF_BAR + S * 8;                    // [2 NWARP] f64
 constexpr int OFF_CUR = OFF_RED + 16 * 8;                   // producer cursor
 constexpr int SMEM_BYTES = OFF_CUR + 128;
@@ -111,6 +113,7 @@ struct Maps {
     CUtensorMap c;     // cell modulus: box [ZP][NWARP][32]
     CUtensorMap p;     // previous iterate: box [3][ZP][W][32]
     CUtensorMap m;     // node mask: box [ZP][W][32]
+    CUtensorMap o;     // output field: box [3][1][W][32] (TMA store, one node plane)
 };
 
 // Producer cursor over the CTA's task sequence: items (b, b+grid, ...), x tiles,
@@ -164,12 +167,11 @@ __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned
 
 // Everything a task needs that is fixed for one x-tile of one item.
 struct Tile {
-    int t;
     bool upd;            // this thread owns a grid node of the tile
-    double ninv;         // -1/V at an interior z plane
-    double ninv_end;     // -1/V at z = 0 or nz-1
-    long long node0;     // lidx(i, j, 0) (loads and pinned values)
-    double* xw;          // x-halo out (lane 31) / in (lane 0)
+    double ninv;         // -1/V at an interior z plane (x2 at z = 0 or nz-1)
+    double ca;           // coefficient of the face sum in the update: c3/dt/1 times ninv
+    long long node0;     // lidx(i, j, 0) (loads, pinned values, peer stores)
+    double* xw;          // x-halo out (lane 31) / in (lane 0; zeros at an item's first tile)
     const double* xr;
 };
 
@@ -287,11 +289,13 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
 }
 
 // Node (i, j, kc): edge sums with warp w-1's shares, inverse x butterflies (x-halo
-// for lane 0), then the residual, the update and the store.  u_n arrives in u.
-template <int FORM>
+// for lane 0), then the residual, the update and the value into the output
+// staging (so, one node plane) -- the producer stores it with TMA.  u_n arrives
+// in u.  RSQ: accumulate r^2 (only the tolerance loop reads it).
+template <int FORM, bool RSQ>
 __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int zi, const double (&Yj)[2][3],
                                      const double* below, const double (&u)[3], const double* sp,
-                                     unsigned char mk, double& rsq, unsigned& bad) {
+                                     unsigned char mk, double* so, double& rsq, unsigned& bad) {
     const int l = threadIdx.x & 31;
     const Geo& g = P.g;
     double Xi[3], Xn[3];
@@ -306,8 +310,9 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
     const double* xr = T.xr + zi * (NWARP * 3);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double nb = __shfl_up_sync(0xffffffffu, Xn[c], 1);
-        acc[c] = Xi[c] + (l > 0 ? nb : (T.t > 0 ? xr[c] : 0.0));
+        double nb = __shfl_up_sync(0xffffffffu, Xn[c], 1);
+        if (l == 0) nb = xr[c];
+        acc[c] = Xi[c] + nb;
     }
     if (l == 31) {
         double* xw = T.xw + zi * (NWARP * 3);
@@ -315,21 +320,26 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
         for (int c = 0; c < 3; ++c) xw[c] = Xn[c];
     }
     if (!T.upd) return;
-    const double ninv = (kc == 0 || kc == g.nz - 1) ? T.ninv_end : T.ninv;  // warp-uniform select
-    auto update = [&](int c, double r) {
-        if (FORM <= 1) return fma(P.c1, u[c], fma(-P.c2, sp[c * PSTRIDE], P.c3 * r));
-        if (FORM == 2) return fma(P.dt, r, u[c]);
-        return r;
-    };
+    const bool endz = kc == 0 || kc == g.nz - 1;  // warp-uniform
     double nv[3];
     if (!mk) {
+        double ca = T.ca, ninv = T.ninv;
+        if (endz) {
+            ca += ca;
+            ninv += ninv;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double r = acc[c] * ninv;
-            nv[c] = update(c, r);
-            rsq = fma(r, r, rsq);
+            if (FORM <= 1) nv[c] = fma(P.c1, u[c], fma(-P.c2, sp[c * PSTRIDE], ca * acc[c]));
+            else if (FORM == 2) nv[c] = fma(ca, acc[c], u[c]);
+            else nv[c] = acc[c] * ninv;
+            if (RSQ) {
+                const double r = acc[c] * ninv;
+                rsq = fma(r, r, rsq);
+            }
         }
     } else {  // rare: pinned components and/or a load on this node
+        const double ninv = endz ? 2.0 * T.ninv : T.ninv;
         const long long node = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -339,27 +349,29 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
             if (pinned) {
                 nv[c] = FORM == 3 ? 0.0 : P.aux[c * g.Ns + node];
             } else {
-                rsq = fma(r, r, rsq);
-                nv[c] = update(c, r);
+                if (RSQ) rsq = fma(r, r, rsq);
+                if (FORM <= 1) nv[c] = fma(P.c1, u[c], fma(-P.c2, sp[c * PSTRIDE], P.c3 * r));
+                else if (FORM == 2) nv[c] = fma(P.dt, r, u[c]);
+                else nv[c] = r;
             }
         }
     }
     // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
     unsigned ex = 0;
-    const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
-    double* dst = P.next + local;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
-        dst[c * g.Ns] = nv[c];
+        so[c * W * 32] = nv[c];
     }
     // a boundary plane is also the neighbour's ghost plane: store it there directly
     // (NVLink / same-device stores, overlapped with the rest of the step)
     if (kc == g.kb && P.peer_lo) {
+        const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
         for (int c = 0; c < 3; ++c) P.peer_lo[c * P.peer_lo_Ns + local] = nv[c];
     }
     if (kc == g.ke - 1 && P.peer_hi) {
+        const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
         for (int c = 0; c < 3; ++c) P.peer_hi[c * P.peer_hi_Ns + local] = nv[c];
     }
@@ -402,7 +414,7 @@ __device__ __forceinline__ void walk(const Params& P, F&& f) {
     }
 }
 
-template <int FORM>
+template <int FORM, bool RSQ>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -420,6 +432,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         prefetch_tmap(&M.c);
         prefetch_tmap(&M.p);
         prefetch_tmap(&M.m);
+        prefetch_tmap(&M.o);
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         pc->item = blockIdx.x;
@@ -489,16 +502,37 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     } else if (w == NWARP) {
         // ------------------------------------------------------------- producer
         regs_shrink<REG_NODE>();
-        uint32_t st = 0;
-        walk(P, [&](bool, int, int, int, int, bool) {
+        uint32_t st = 0, q = 0;
+        // the node output of the previous task (stored once the node warps are done with it)
+        bool pown = false, ptwo = false;
+        int pi0 = 0, pj0 = 0, pk = 0;
+        auto store_prev = [&]() {
+            if (l == 0 && pown) {
+                const double* so = reinterpret_cast<const double*>(smem + OFF_O) + ((q - 1) & 1) * (ZP * OSTRIDE);
+                tma_store_4d(&M.o, so, pi0, pj0, pk, 0);
+                if (ptwo) tma_store_4d(&M.o, so + OSTRIDE, pi0, pj0, pk + 1, 0);
+                bulk_commit();
+            }
+        };
+        walk(P, [&](bool own, int s, int t, int, int kc, bool two) {
+            if (l == 0) bulk_wait_read_all();  // staging (q-2) & 1 is free before the node warps refill it
             __syncthreads();  // cell warps done with task q, node warps with task q-1
             if (l == 0 && pc->valid) {  // refill the stage of task q-1
                 issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
                 pc->next(P);
             }
+            store_prev();
+            pown = own;
+            ptwo = two;
+            pi0 = t * 32;
+            pj0 = s * W;
+            pk = kc - g.ks0;
+            ++q;
             if (++st == S) st = 0;
         });
         __syncthreads();
+        store_prev();
+        if (l == 0) bulk_wait_all();
     } else {
         // ------------------------------------------------------------ node warps
         regs_shrink<REG_NODE>();
@@ -507,21 +541,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         uint32_t st = 0, q = 0;
         const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
         Tile T{};  // set at each x tile's prologue task
+        int ntile = 0;
         walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
             __syncthreads();  // the cell warps finished task q
             tmem_fence_after();
             const unsigned char* sb = smem + st * STAGE_BYTES;
             const double* su = reinterpret_cast<const double*>(sb + OFF_U) + v * BOXX + l;  // plane 0, row v
             if (!own) {
-                T.t = t;
                 const int i = t * 32 + l, j = s * W - 1 + v;
                 T.upd = i < g.nx && j < g.ny;
                 const int ends = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
                 T.ninv = -P.inv_base * (double)(1 << ends);
-                T.ninv_end = 2.0 * T.ninv;
+                T.ca = (FORM <= 1 ? P.c3 : FORM == 2 ? P.dt : 1.0) * T.ninv;
                 T.node0 = (long long)j * g.px + i;
-                T.xw = sX + (t & 1) * (LMAX * NWARP * 3) + v * 3;
-                T.xr = sX + ((t + 1) & 1) * (LMAX * NWARP * 3) + v * 3;
+                // x-halo buffers alternate per tile of the CTA; the first tile of an
+                // item reads zeros (no cell to the left of x = 0)
+                T.xw = sX + (ntile & 1) * (LMAX * NWARP * 3) + v * 3;
+                T.xr = sX + ((ntile + 1) & 1) * (LMAX * NWARP * 3) + v * 3;
+                if (t == 0) {
+                    for (int k = l; k < LMAX * 3; k += 32) const_cast<double*>(T.xr)[(k / 3) * (NWARP * 3) + k % 3] = 0.0;
+                    __syncwarp();
+                }
+                ++ntile;
             } else {
                 double Yv[12];
                 tmem_ld12(tq + (q & 1) * 32, Yv);
@@ -530,14 +571,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 const double* below = sY + (q & 1) * (NWARP * YS) + (v - 1) * YS + l;
                 const unsigned char* mk = sb + OFF_M + (v - 1) * 32 + l;
                 const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (v - 1) * 32 + l;
-                node<FORM>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], rsq, bad);
+                double* so = reinterpret_cast<double*>(smem + OFF_O) + (q & 1) * (ZP * OSTRIDE) + (v - 1) * 32 + l;
+                node<FORM, RSQ>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], so, rsq, bad);
                 if (two) {
                     double u1[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
-                    node<FORM>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32], rsq,
-                               bad);
+                    node<FORM, RSQ>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32],
+                                    so + OSTRIDE, rsq, bad);
                 }
+                fence_async_smem();  // the staging is read by the producer's TMA store
             }
             // u_n of the next task's first node plane (stage plane 1)
 #pragma unroll

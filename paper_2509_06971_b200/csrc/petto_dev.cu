@@ -195,9 +195,12 @@ int make_tmaps(petto_ctx* ctx) {
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
+    const cuuint32_t boxO[4] = {32, e3::W, 1, 3};
     for (int b = 0; b < 3; ++b)
-        if (!map4(&ctx->tU[b], ctx->st[b], boxU) || !map4(&ctx->tP[b], ctx->st[b], boxP))
+        if (!map4(&ctx->tU[b], ctx->st[b], boxU) || !map4(&ctx->tP[b], ctx->st[b], boxP) ||
+            !map4(&ctx->tO[b], ctx->st[b], boxO))
             return fail(ctx, PETTO_ERROR, "tensor map (state) encode failed");
+    if (!map4(&ctx->tO[3], ctx->r, boxO)) return fail(ctx, PETTO_ERROR, "tensor map (residual) encode failed");
     const cuuint64_t d3[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs};
     const cuuint64_t s3[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8};
     const cuuint32_t boxC[3] = {32, e3::NWARP, e3::ZP};
@@ -448,6 +451,13 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             M.c = ctx->tC;
             M.p = ctx->tP[prev];
             M.m = ctx->tM;
+            {
+                int ob = next == ctx->r ? 3 : -1;
+                for (int b = 0; b < 3; ++b)
+                    if (next == ctx->st[b]) ob = b;
+                if (ob < 0) return fail(ctx, PETTO_ERROR, "fused 3D step: output is not a context buffer");
+                M.o = ctx->tO[ob];
+            }
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
             cfg.blockDim = dim3(e3::WS_THREADS);
@@ -455,11 +465,16 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             cfg.stream = ctx->stream;
             timing_begin(ctx, ev);
             cudaError_t le;
-            switch (k.form) {
-                case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0>, P, M); break;
-                case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1>, P, M); break;
-                case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2>, P, M); break;
-                default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3>, P, M); break;
+            // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
+            switch (k.form * 2 + (partials ? 1 : 0)) {
+                case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false>, P, M); break;
+                case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, true>, P, M); break;
+                case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false>, P, M); break;
+                case 3: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, true>, P, M); break;
+                case 4: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false>, P, M); break;
+                case 5: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, true>, P, M); break;
+                case 6: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, false>, P, M); break;
+                default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true>, P, M); break;
             }
             if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
             timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
@@ -721,10 +736,14 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
 #define E3_KERNEL e3::k_elastic3d_fast
-    if (cudaFuncSetAttribute(E3_KERNEL<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<3>, smattr, e3::SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(E3_KERNEL<0, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<0, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, true>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");

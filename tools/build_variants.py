@@ -26,8 +26,10 @@ def one(spec):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         return f"{name}: FAILED\n{r.stderr[-2000:]}"
-    m = re.search(r"k_elastic3d_fastILi1E.*?\n(.*?spill.*?)\n.*?Used (\d+) registers", r.stderr, re.S)
-    return f"{name}: {m.group(2)} regs, {m.group(1).strip()}" if m else f"{name}: built"
+    out = []
+    for m in re.finditer(r"Compiling entry function '\S*k_elastic3d_fastILi(\d)ELb(\d)E.*?\n(?:.*?\n)*?(.*?spill.*?)\n.*?Used (\d+) registers", r.stderr):
+        out.append(f"<{m.group(1)},{m.group(2)}> {m.group(4)} regs {m.group(3).strip()}")
+    return f"{name}: " + ("; ".join(out) if out else "built")
 
 
 if __name__ == "__main__":
