@@ -36,6 +36,8 @@
 // u_{n+1} 24 (+1 mask byte); PT drops u_{n-1}.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace petto_b200 {
@@ -167,7 +169,7 @@ __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned
 
 // Everything a task needs that is fixed for one x-tile of one item.
 struct Tile {
-    bool upd;            // this thread owns a grid node of the tile
+    bool upd;            // this thread owns a grid node of the tile (peer stores)
     double ninv;         // -1/V at an interior z plane (x2 at z = 0 or nz-1)
     double ca;           // coefficient of the face sum in the update: c3/dt/1 times ninv
     long long node0;     // lidx(i, j, 0) (loads, pinned values, peer stores)
@@ -291,11 +293,14 @@ __device__ __forceinline__ void cell(const Params& P, const double (&Bc)[4][3], 
 // Node (i, j, kc): edge sums with warp w-1's shares, inverse x butterflies (x-halo
 // for lane 0), then the residual, the update and the value into the output
 // staging (so, one node plane) -- the producer stores it with TMA.  u_n arrives
-// in u.  RSQ: accumulate r^2 (only the tolerance loop reads it).
-template <int FORM, bool RSQ>
+// in u.  RSQ: accumulate r^2 (only the tolerance loop reads it).  ZEND: the task
+// holds the plane z = 0 or nz-1 (twice the volume weight there).  exm: running
+// minimum of (~hi & exponent mask) over the values written -- 0 iff one of them
+// is not finite.
+template <int FORM, bool RSQ, bool ZEND>
 __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int zi, const double (&Yj)[2][3],
                                      const double* below, const double (&u)[3], const double* sp,
-                                     unsigned char mk, double* so, double& rsq, unsigned& bad) {
+                                     unsigned char mk, double* so, double& rsq, unsigned& exm) {
     const int l = threadIdx.x & 31;
     const Geo& g = P.g;
     double Xi[3], Xn[3];
@@ -319,12 +324,13 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
 #pragma unroll
         for (int c = 0; c < 3; ++c) xw[c] = Xn[c];
     }
-    if (!T.upd) return;
-    const bool endz = kc == 0 || kc == g.nz - 1;  // warp-uniform
+    // nodes outside the grid (TMA zero-filled inputs, zero cell moduli) compute 0.0;
+    // the TMA store clips them
+    const bool endz = ZEND && (kc == 0 || kc == g.nz - 1);  // warp-uniform
     double nv[3];
     if (!mk) {
         double ca = T.ca, ninv = T.ninv;
-        if (endz) {
+        if (ZEND && endz) {
             ca += ca;
             ninv += ninv;
         }
@@ -357,25 +363,23 @@ __device__ __forceinline__ void node(const Params& P, const Tile& T, int kc, int
         }
     }
     // non-finite iff the exponent field is all ones (integer pipe, no FP64 work)
-    unsigned ex = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        ex |= ((__double2hiint(nv[c]) & 0x7ff00000) == 0x7ff00000);
+        exm = min(exm, ~(unsigned)__double2hiint(nv[c]) & 0x7ff00000u);
         so[c * W * 32] = nv[c];
     }
     // a boundary plane is also the neighbour's ghost plane: store it there directly
     // (NVLink / same-device stores, overlapped with the rest of the step)
-    if (kc == g.kb && P.peer_lo) {
+    if (kc == g.kb && P.peer_lo && T.upd) {
         const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
         for (int c = 0; c < 3; ++c) P.peer_lo[c * P.peer_lo_Ns + local] = nv[c];
     }
-    if (kc == g.ke - 1 && P.peer_hi) {
+    if (kc == g.ke - 1 && P.peer_hi && T.upd) {
         const long long local = T.node0 + (long long)(kc - g.ks0) * g.ny * g.px;
 #pragma unroll
         for (int c = 0; c < 3; ++c) P.peer_hi[c * P.peer_hi_Ns + local] = nv[c];
     }
-    bad |= ex;
 }
 
 // ---------------------------------------------------------------------------
@@ -542,6 +546,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
         Tile T{};  // set at each x tile's prologue task
         int ntile = 0;
+        unsigned exm = 0xffffffffu;
         walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
             __syncthreads();  // the cell warps finished task q
             tmem_fence_after();
@@ -572,14 +577,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 const unsigned char* mk = sb + OFF_M + (v - 1) * 32 + l;
                 const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (v - 1) * 32 + l;
                 double* so = reinterpret_cast<double*>(smem + OFF_O) + (q & 1) * (ZP * OSTRIDE) + (v - 1) * 32 + l;
-                node<FORM, RSQ>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], so, rsq, bad);
-                if (two) {
-                    double u1[3];
+                auto planes = [&](auto zend) {
+                    constexpr bool ZE = decltype(zend)::value;
+                    node<FORM, RSQ, ZE>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], so, rsq, exm);
+                    if (two) {
+                        double u1[3];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
-                    node<FORM, RSQ>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32, mk[W * 32],
-                                    so + OSTRIDE, rsq, bad);
-                }
+                        for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
+                        node<FORM, RSQ, ZE>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32,
+                                            mk[W * 32], so + OSTRIDE, rsq, exm);
+                    }
+                };
+                if (kc == 0 || kc + 1 >= g.nz - 1) planes(std::true_type{});
+                else planes(std::false_type{});
                 fence_async_smem();  // the staging is read by the producer's TMA store
             }
             // u_n of the next task's first node plane (stage plane 1)
@@ -589,6 +599,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             if (++st == S) st = 0;
         });
         if (P.peer_lo || P.peer_hi) __threadfence_system();  // peer stores before the step's signal
+        bad = exm == 0;
         __syncthreads();
     }
 
