@@ -204,11 +204,10 @@ __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fenc
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// four doubles (eight columns) per thread
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, double a, double b, double c, double d) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
-                 "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)), "r"(__double2hiint(b)),
-                 "r"(__double2loint(c)), "r"(__double2hiint(c)), "r"(__double2loint(d)), "r"(__double2hiint(d))
+// one double (two columns) per thread: a register pair as it is, no marshalling
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, double a) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__double2loint(a)),
+                 "r"(__double2hiint(a))
                  : "memory");
 }
 // twelve doubles (24 columns at taddr): three loads and the wait in one block, so

@@ -488,9 +488,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
                 if (w > 0) {  // the y-halo row's own sums are not needed
                     const uint32_t ta = tq + (q & 1) * 32;
-                    tmem_st4(ta, Y0[0][0], Y0[0][1], Y0[0][2], Y0[1][0]);
-                    tmem_st4(ta + 8, Y0[1][1], Y0[1][2], Y1[0][0], Y1[0][1]);
-                    tmem_st4(ta + 16, Y1[0][2], Y1[1][0], Y1[1][1], Y1[1][2]);
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) {
+                        tmem_st1(ta + 2 * k, Y0[k / 3][k % 3]);
+                        tmem_st1(ta + 12 + 2 * k, Y1[k / 3][k % 3]);
+                    }
                     tmem_wait_st();
                 }
             }
