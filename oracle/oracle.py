@@ -413,6 +413,22 @@ class Oracle:
                                      recs, records_cap, C.byref(nrec), C.byref(res)))
         return phases, state, [recs[i] for i in range(min(nrec.value, records_cap))], res
 
+    # -- output writers (field_io.cpp) ----------------------------------------
+    def write_field_csv(self, grid, values, path):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self.lib.orc_write_field_csv(C.byref(grid_struct(grid).c), _dp(v), str(path).encode()))
+
+    def write_pgm(self, grid, values, path):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self.lib.orc_write_pgm(C.byref(grid_struct(grid).c), _dp(v), str(path).encode()))
+
+    def write_vtk(self, grid, arrays, path):
+        """arrays: list of (name, values) in file order."""
+        names = (C.c_char_p * len(arrays))(*[n.encode() for n, _ in arrays])
+        vals = np.ascontiguousarray(np.concatenate([np.asarray(v, dtype=np.float64) for _, v in arrays]))
+        self._check(self.lib.orc_write_vtk(C.byref(grid_struct(grid).c), len(arrays), names, _dp(vals),
+                                           str(path).encode()))
+
 
 _cache = {}
 

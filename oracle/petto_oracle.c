@@ -1400,3 +1400,92 @@ done:
     free(comp_hist);
     return rc;
 }
+
+/* ------------------------------------------------------------------ writers */
+/* field_io.cpp:15-19: every double through snprintf("%.17g"). */
+static int io_fail(const char* what, const char* path) {
+    char m[600];
+    snprintf(m, sizeof m, "%s '%s'%s", what, path, strcmp(what, "cannot open") == 0 ? " for writing" : "");
+    return fail(4, m);
+}
+
+/* write_field_csv (field_io.cpp:29-47): header line, then one line per (k, j) row. */
+int orc_write_field_csv(const orc_grid* o, const double* values, const char* path) {
+    grid_t g;
+    if (grid_init(&g, o)) return 2;
+    FILE* f = fopen(path, "w");
+    if (!f) return io_fail("cannot open", path);
+    fprintf(f, "# nx=%lld ny=%lld nz=%lld dx=%.17g dy=%.17g dz=%.17g\n", (long long)g.n[0], (long long)g.n[1],
+            (long long)g.n[2], g.h[0], g.h[1], g.h[2]);
+    for (int64_t k = 0; k < g.n[2]; ++k)
+        for (int64_t j = 0; j < g.n[1]; ++j) {
+            const int64_t row = (k * g.n[1] + j) * g.n[0];
+            for (int64_t i = 0; i < g.n[0]; ++i) fprintf(f, i ? ",%.17g" : "%.17g", values[row + i]);
+            fputc('\n', f);
+        }
+    const int bad = ferror(f);
+    if (fclose(f) || bad) return io_fail("write failed for", path);
+    return 0;
+}
+
+/* write_pgm (field_io.cpp:68-101): finite min/max, rows top-down, lround(255 v). */
+int orc_write_pgm(const orc_grid* o, const double* values, const char* path) {
+    grid_t g;
+    if (grid_init(&g, o)) return 2;
+    if (g.dim != 2) return fail(2, "write_pgm: only 2D fields");
+    const int64_t n = nnodes(&g);
+    double lo = 0.0, hi = 0.0;
+    int first = 1;
+    for (int64_t i = 0; i < n; ++i) {
+        const double v = values[i];
+        if (!isfinite(v)) continue;
+        lo = first ? v : (v < lo ? v : lo); /* std::min(lo, v): lo unless v < lo */
+        hi = first ? v : (hi < v ? v : hi); /* std::max(hi, v): hi unless hi < v */
+        first = 0;
+    }
+    const double span = hi > lo ? hi - lo : 1.0;
+    FILE* f = fopen(path, "wb");
+    if (!f) return io_fail("cannot open", path);
+    fprintf(f, "P5\n%lld %lld\n255\n", (long long)g.n[0], (long long)g.n[1]);
+    unsigned char* row = (unsigned char*)malloc((size_t)g.n[0]);
+    for (int64_t j = g.n[1] - 1; j >= 0; --j) {
+        for (int64_t i = 0; i < g.n[0]; ++i) {
+            const double raw = values[j * g.n[0] + i];
+            const double v = isfinite(raw) ? (raw - lo) / span : 0.0;
+            const double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); /* std::clamp */
+            row[i] = (unsigned char)lround(255.0 * c);
+        }
+        fwrite(row, 1, (size_t)g.n[0], f);
+    }
+    free(row);
+    const int bad = ferror(f);
+    if (fclose(f) || bad) return io_fail("write failed for", path);
+    char side[1100];
+    snprintf(side, sizeof side, "%s.scale.txt", path);
+    FILE* s = fopen(side, "w");
+    if (!s) return fail(4, "cannot open side file for writing");
+    fprintf(s, "min = %.17g\nmax = %.17g\nrows = top_to_bottom\n", lo, hi);
+    fclose(s);
+    return 0;
+}
+
+/* write_vtk_structured_points (field_io.cpp:103-126): legacy ASCII, one value per line. */
+int orc_write_vtk(const orc_grid* o, int narrays, const char* const* names, const double* values,
+                  const char* path) {
+    grid_t g;
+    if (grid_init(&g, o)) return 2;
+    FILE* f = fopen(path, "w");
+    if (!f) return io_fail("cannot open", path);
+    const int64_t n = nnodes(&g);
+    fprintf(f,
+            "# vtk DataFile Version 3.0\nstructured point fields\nASCII\nDATASET STRUCTURED_POINTS\n"
+            "DIMENSIONS %lld %lld %lld\nORIGIN 0 0 0\nSPACING %.17g %.17g %.17g\nPOINT_DATA %lld\n",
+            (long long)g.n[0], (long long)g.n[1], (long long)g.n[2], g.h[0], g.h[1], g.h[2], (long long)n);
+    for (int a = 0; a < narrays; ++a) {
+        fprintf(f, "SCALARS %s double 1\nLOOKUP_TABLE default\n", names[a]);
+        for (int64_t i = 0; i < n; ++i) fprintf(f, "%.17g\n", values[(int64_t)a * n + i]);
+    }
+    const int bad = ferror(f);
+    if (fclose(f) || bad) return io_fail("write failed for", path);
+    return 0;
+}

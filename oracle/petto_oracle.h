@@ -190,6 +190,15 @@ int orc_run(const orc_problem* prob, const orc_schedule* sched, double* phases_o
             double* state_out, orc_record* records, long records_cap, long* nrecords,
             orc_run_result* result);
 
+/* Output writers (field_io.cpp): write_field_csv (:29-47), write_pgm (:68-101,
+ * 2D only, plus "<path>.scale.txt"), write_vtk_structured_points (:103-126) with
+ * narrays consecutive N-blocks named names[i].  Errors: 2 invalid argument,
+ * 4 IoError (cannot open / write failed). */
+int orc_write_field_csv(const orc_grid* g, const double* values, const char* path);
+int orc_write_pgm(const orc_grid* g, const double* values, const char* path);
+int orc_write_vtk(const orc_grid* g, int narrays, const char* const* names, const double* values,
+                  const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@
 #include <vector>
 
 #include "petto/config_io.hpp"
+#include "petto/errors.hpp"
+#include "petto/field_io.hpp"
 #include "petto/engine.hpp"
 #include "petto/objectives.hpp"
 #include "petto/optimizer.hpp"
@@ -112,6 +114,24 @@ int guarded(F&& fn) {
     } catch (const NumericalAbort& e) {
         g_err = e.what();
         return 1;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// IoError -> 4 (the CLI's exit code for it, src/engine.cpp:259-268)
+template <class F>
+int guarded_io(F&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 4;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return 2;
@@ -539,6 +559,32 @@ const char* ref_config_json(const char* text) {
     });
     if (rc) g_json = std::string("{\"error\": ") + std::to_string(rc) + "}";
     return g_json.c_str();
+}
+
+int orc_write_field_csv(const orc_grid* g, const double* values, const char* path) {
+    return guarded_io([&] {
+        const Grid grid = make_grid(g);
+        write_field_csv(grid, std::vector<double>(values, values + grid.num_nodes()), path);
+    });
+}
+
+int orc_write_pgm(const orc_grid* g, const double* values, const char* path) {
+    return guarded_io([&] {
+        const Grid grid = make_grid(g);
+        write_pgm(grid, std::vector<double>(values, values + grid.num_nodes()), path);
+    });
+}
+
+int orc_write_vtk(const orc_grid* g, int narrays, const char* const* names, const double* values,
+                  const char* path) {
+    return guarded_io([&] {
+        const Grid grid = make_grid(g);
+        const Index n = grid.num_nodes();
+        std::vector<std::pair<std::string, std::vector<double>>> arrays;
+        for (int a = 0; a < narrays; ++a)
+            arrays.emplace_back(names[a], std::vector<double>(values + a * n, values + (a + 1) * n));
+        write_vtk_structured_points(grid, arrays, path);
+    });
 }
 
 }  // extern "C"
