@@ -35,6 +35,7 @@ extern "C" {
 #define PETTO_ABORT 1
 #define PETTO_INVALID 2
 #define PETTO_ERROR 3
+#define PETTO_IO 4  /* IoError (errors.hpp): cannot open / write failed (CLI exit code 4) */
 
 #define PETTO_MAX_PHASES 8
 
@@ -254,6 +255,32 @@ double petto_dev_spectral_bound(int dim, const int64_t n[3], const double length
 
 /* Instrumentation for bench.py: kernel launches issued by this context, and
  * (when enabled) CUDA-event time of the dominant state kernel. */
+/* ---- Output writers --------------------------------
+ * The reference's writers from device buffers, byte-identical to its files:
+ * every value formatted on the device exactly as snprintf("%.17g")
+ * (field_io.cpp:15-19), the text assembled in HBM and written in chunks.
+ * Single-domain contexts only (a slab rank returns PETTO_INVALID).  Errors:
+ * PETTO_IO with the reference's IoError message. */
+#define PETTO_FIELD_STATE 0    /* component `index` of the current state */
+#define PETTO_FIELD_PHASE 1    /* phase `index` (after petto_dev_set_design) */
+#define PETTO_FIELD_PROPERTY 2 /* the property field (E / kappa; petto_dev_interpolate refreshes it) */
+typedef struct {
+    int field;
+    int index;
+    const char* name;  /* VTK array name, e.g. "phase_0", "modulus", "displacement_x" */
+} petto_array;
+/* write_field_csv (field_io.cpp:29-47) */
+int petto_dev_write_field_csv(petto_ctx* ctx, int field, int index, const char* path);
+/* write_vtk_structured_points (field_io.cpp:103-126), arrays in file order */
+int petto_dev_write_vtk(petto_ctx* ctx, const petto_array* arrays, int narrays, const char* path);
+/* write_pgm (field_io.cpp:68-101), 2D only; also writes "<path>.scale.txt" */
+int petto_dev_write_pgm(petto_ctx* ctx, int field, int index, const char* path);
+/* The formatter alone: n doubles (host or device memory) as "%.17g" each followed
+ * by '\n' (sep_mode 0) or by ',' / '\n' at the end of every `row` values
+ * (sep_mode 1) into out[0, cap); *len = bytes written. */
+int petto_dev_format_values(petto_ctx* ctx, const double* values, int64_t n, int sep_mode, int64_t row,
+                            char* out, int64_t cap, int64_t* len);
+
 int64_t petto_dev_launch_count(const petto_ctx* ctx);
 int petto_dev_kernel_timing(petto_ctx* ctx, int enable);
 int petto_dev_kernel_stats(petto_ctx* ctx, double* total_ms, int64_t* launches,

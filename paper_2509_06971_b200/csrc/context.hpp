@@ -110,6 +110,16 @@ struct petto_ctx {
     cudaEvent_t ev_step = nullptr;   // local group: this context's step finished
     cudaEvent_t ev_pull = nullptr;   // local group: this context's ghost pulls finished
 
+    // output writers (writers.cuh): two text buffers on each side for the
+    // format -> copy -> write pipeline, per-block byte counts / offsets, scan scratch
+    char* wtext[2] = {nullptr, nullptr};
+    char* htext[2] = {nullptr, nullptr};  // pinned
+    long long* wblk = nullptr;            // [2 * blocks]: bytes per block, then offsets
+    long long* wcount = nullptr;          // pinned [2]: text bytes of the chunk in each buffer
+    void* wscan = nullptr;
+    size_t wscan_bytes = 0;
+    void* wmm = nullptr;                  // PGM min/max partials
+
     // instrumentation
     long long launches = 0;
     bool timing = false;

@@ -25,6 +25,9 @@
 #include "fast2d.cuh"
 #include "replica.cuh"
 #include "stiffness.hpp"
+#include "writers.cuh"
+
+#include <cub/device/device_scan.cuh>
 
 using namespace petto_b200;
 
@@ -655,6 +658,128 @@ int check_kappa(petto_ctx* ctx) {
 
 // ======================================================================= C-ABI
 
+namespace {
+constexpr long long WCHUNK = 8LL << 20;  // values per chunk
+constexpr long long WBLOCKS = WCHUNK / wr::TB;
+
+int writer_buffers(petto_ctx* ctx) {
+    if (ctx->wtext[0]) return PETTO_OK;
+    const size_t cap = (size_t)WCHUNK * wr::MAXB;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&ctx->wtext[b], cap));
+        CK(cudaMallocHost(&ctx->htext[b], cap));
+    }
+    CK(cudaMalloc(&ctx->wblk, sizeof(long long) * 2 * (WBLOCKS + 1)));
+    CK(cudaMallocHost(&ctx->wcount, sizeof(long long) * 2));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, ctx->wscan_bytes, ctx->wblk, ctx->wblk, (int)(WBLOCKS + 1)));
+    CK(cudaMalloc(&ctx->wscan, ctx->wscan_bytes));
+    return PETTO_OK;
+}
+
+// The field a writer reads: component/phase `index` of the context's state,
+// phases or property, in the reference's node order.
+int writer_source(petto_ctx* ctx, int field, int index, wr::Src* out) {
+    const Geo& g = ctx->g;
+    if (g.kb != 0 || g.ke != g.nz)
+        return fail(ctx, PETTO_INVALID, "writers need the whole grid in one context (slab rank: gather first)");
+    const double* base = nullptr;
+    if (field == PETTO_FIELD_STATE) {
+        if (index < 0 || index >= ctx->comps) return fail(ctx, PETTO_INVALID, "writer: state component out of range");
+        base = ctx->st[ctx->cur] + (long long)index * g.Ns;
+    } else if (field == PETTO_FIELD_PHASE) {
+        if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+        if (index < 0 || index >= ctx->mat.nphases) return fail(ctx, PETTO_INVALID, "writer: phase out of range");
+        base = ctx->phases + (long long)index * g.Ns;
+    } else if (field == PETTO_FIELD_PROPERTY) {
+        base = ctx->prop;
+    } else {
+        return fail(ctx, PETTO_INVALID, "writer: unknown field");
+    }
+    *out = wr::Src{base, g.nx, g.ny, g.px, (long long)g.px * g.ny, (long long)g.nx * g.ny * g.nz};
+    return PETTO_OK;
+}
+
+// Formats src's values ("%.17g" + separator) chunk by chunk and hands the bytes
+// to sink(const char*, size_t) in order.
+template <class Sink>
+int format_stream(petto_ctx* ctx, const wr::Src& src, int sep_mode, Sink&& sink) {
+    if (int rc = writer_buffers(ctx)) return rc;
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    int rc = PETTO_OK;
+    long long c = 0;
+    for (long long i0 = 0; i0 < src.n && rc == PETTO_OK; i0 += WCHUNK, ++c) {
+        const int b = (int)(c & 1);
+        const long long n = std::min(WCHUNK, src.n - i0);
+        const int blocks = (int)((n + wr::TB - 1) / wr::TB);
+        long long* bytes = ctx->wblk + (size_t)b * (WBLOCKS + 1);
+        wr::k_block_bytes<<<blocks, wr::TB, 0, ctx->stream>>>(src, i0, n, bytes);
+        cudaMemsetAsync(bytes + blocks, 0, sizeof(long long), ctx->stream);
+        size_t tb = ctx->wscan_bytes;
+        // exclusive scan in place: bytes[blocks] becomes the chunk's total
+        if (cub::DeviceScan::ExclusiveSum(ctx->wscan, tb, bytes, bytes, blocks + 1, ctx->stream) != cudaSuccess) {
+            rc = fail(ctx, PETTO_ERROR, "writer: scan failed");
+            break;
+        }
+        wr::k_block_write<<<blocks, wr::TB, 0, ctx->stream>>>(src, i0, n, sep_mode, bytes, ctx->wtext[b]);
+        ctx->launches += 3;
+        if (cudaGetLastError() != cudaSuccess) {
+            rc = fail(ctx, PETTO_ERROR, "writer: launch failed");
+            break;
+        }
+        cudaMemcpyAsync(&ctx->wcount[b], bytes + blocks, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(ctx->htext[b], ctx->wtext[b], (size_t)n * wr::MAXB, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaEventRecord(ev[b], ctx->stream);
+        if (c > 0) {  // the previous chunk while this one formats and copies
+            cudaEventSynchronize(ev[1 - b]);
+            rc = sink(ctx->htext[1 - b], (size_t)ctx->wcount[1 - b]);
+        }
+    }
+    if (rc == PETTO_OK && c > 0) {
+        const int b = (int)((c - 1) & 1);
+        if (cudaEventSynchronize(ev[b]) != cudaSuccess) rc = fail(ctx, PETTO_ERROR, "writer: copy failed");
+        else rc = sink(ctx->htext[b], (size_t)ctx->wcount[b]);
+    }
+    cudaStreamSynchronize(ctx->stream);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return rc;
+}
+
+std::string fmt17(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+
+struct OutFile {
+    FILE* f = nullptr;
+    ~OutFile() {
+        if (f) std::fclose(f);
+    }
+};
+
+int open_out(petto_ctx* ctx, OutFile& o, const char* path, bool binary) {
+    o.f = std::fopen(path, binary ? "wb" : "w");
+    if (!o.f) return fail(ctx, PETTO_IO, std::string("cannot open '") + path + "' for writing");
+    std::setvbuf(o.f, nullptr, _IOFBF, 1 << 22);
+    return PETTO_OK;
+}
+
+int close_out(petto_ctx* ctx, OutFile& o, const char* path) {
+    const bool bad = std::ferror(o.f) != 0;
+    const int rc = std::fclose(o.f);
+    o.f = nullptr;
+    if (bad || rc) return fail(ctx, PETTO_IO, std::string("write failed for '") + path + "'");
+    return PETTO_OK;
+}
+
+std::string grid_dims(const Geo& g) {
+    return std::to_string(g.nx) + " " + std::to_string(g.ny) + " " + std::to_string(g.nz);
+}
+}  // namespace
+
 extern "C" {
 
 const char* petto_dev_version(void) { return "petto_b200 0.1 (sm_100a)"; }
@@ -780,6 +905,14 @@ void petto_dev_destroy(petto_ctx* ctx) {
     cudaFree(ctx->status);
     cudaFree(ctx->dscal);
     if (ctx->status_h) cudaFreeHost(ctx->status_h);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(ctx->wtext[b]);
+        if (ctx->htext[b]) cudaFreeHost(ctx->htext[b]);
+    }
+    cudaFree(ctx->wblk);
+    if (ctx->wcount) cudaFreeHost(ctx->wcount);
+    cudaFree(ctx->wscan);
+    cudaFree(ctx->wmm);
     design_free(ctx);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1832,6 +1965,126 @@ int petto_dev_kernel_stats(petto_ctx* ctx, double* total_ms, int64_t* launches, 
     if (bytes_per_launch) *bytes_per_launch = ctx->bytes_per_launch;
     if (name && name_cap > 0) std::snprintf(name, (size_t)name_cap, "%s", ctx->kernel_name.c_str());
     return PETTO_OK;
+}
+
+
+// ------------------------------------------------------------------ writers
+// the reference's writers (field_io.cpp:29-126) from
+// device buffers, byte-identical.  Values are formatted on the device
+// (writers.cuh); chunks of WCHUNK values alternate between two text buffers so
+// that the copy of chunk c and the host write of chunk c-1 overlap.
+
+int petto_dev_format_values(petto_ctx* ctx, const double* values, int64_t n, int sep_mode, int64_t row,
+                            char* out, int64_t cap, int64_t* len) {
+    CK(cudaSetDevice(ctx->device));
+    if (n < 0 || row <= 0 || (sep_mode != 0 && sep_mode != 1))
+        return fail(ctx, PETTO_INVALID, "format_values: bad arguments");
+    cudaPointerAttributes at{};
+    const bool dev = cudaPointerGetAttributes(&at, values) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    double* tmp = nullptr;
+    if (!dev && n) {
+        CK(cudaMalloc(&tmp, sizeof(double) * (size_t)n));
+        CK(cudaMemcpyAsync(tmp, values, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (sep_mode == 1 && row > (1LL << 30)) return fail(ctx, PETTO_INVALID, "format_values: row too long");
+    const long long nx = sep_mode == 1 ? row : (1LL << 20);  // the separator of mode 0 ignores rows
+    const wr::Src src{dev ? values : tmp, (int)nx, 1, nx, nx, (long long)n};
+    int64_t used = 0;
+    const int rc = format_stream(ctx, src, sep_mode, [&](const char* p, size_t k) {
+        if (used + (int64_t)k > cap) return fail(ctx, PETTO_INVALID, "format_values: output buffer too small");
+        std::memcpy(out + used, p, k);
+        used += (int64_t)k;
+        return PETTO_OK;
+    });
+    cudaFree(tmp);
+    if (len) *len = used;
+    return rc;
+}
+
+int petto_dev_write_field_csv(petto_ctx* ctx, int field, int index, const char* path) {
+    CK(cudaSetDevice(ctx->device));
+    wr::Src src;
+    if (int rc = writer_source(ctx, field, index, &src)) return rc;
+    const Geo& g = ctx->g;
+    OutFile o;
+    if (int rc = open_out(ctx, o, path, false)) return rc;
+    const std::string head = "# nx=" + std::to_string(g.nx) + " ny=" + std::to_string(g.ny) +
+                             " nz=" + std::to_string(g.nz) + " dx=" + fmt17(g.h[0]) + " dy=" + fmt17(g.h[1]) +
+                             " dz=" + fmt17(g.h[2]) + "\n";
+    std::fwrite(head.data(), 1, head.size(), o.f);
+    if (int rc = format_stream(ctx, src, 1, [&](const char* p, size_t k) {
+            std::fwrite(p, 1, k, o.f);
+            return PETTO_OK;
+        }))
+        return rc;
+    return close_out(ctx, o, path);
+}
+
+int petto_dev_write_vtk(petto_ctx* ctx, const petto_array* arrays, int narrays, const char* path) {
+    CK(cudaSetDevice(ctx->device));
+    std::vector<wr::Src> src((size_t)std::max(narrays, 0));
+    for (int a = 0; a < narrays; ++a)
+        if (int rc = writer_source(ctx, arrays[a].field, arrays[a].index, &src[a])) return rc;
+    const Geo& g = ctx->g;
+    OutFile o;
+    if (int rc = open_out(ctx, o, path, false)) return rc;
+    const std::string head = "# vtk DataFile Version 3.0\nstructured point fields\nASCII\nDATASET STRUCTURED_POINTS\n"
+                             "DIMENSIONS " + grid_dims(g) + "\nORIGIN 0 0 0\nSPACING " + fmt17(g.h[0]) + " " +
+                             fmt17(g.h[1]) + " " + fmt17(g.h[2]) + "\nPOINT_DATA " +
+                             std::to_string((long long)g.nx * g.ny * g.nz) + "\n";
+    std::fwrite(head.data(), 1, head.size(), o.f);
+    for (int a = 0; a < narrays; ++a) {
+        const std::string sh = std::string("SCALARS ") + arrays[a].name + " double 1\nLOOKUP_TABLE default\n";
+        std::fwrite(sh.data(), 1, sh.size(), o.f);
+        if (int rc = format_stream(ctx, src[a], 0, [&](const char* p, size_t k) {
+                std::fwrite(p, 1, k, o.f);
+                return PETTO_OK;
+            }))
+            return rc;
+    }
+    return close_out(ctx, o, path);
+}
+
+int petto_dev_write_pgm(petto_ctx* ctx, int field, int index, const char* path) {
+    CK(cudaSetDevice(ctx->device));
+    const Geo& g = ctx->g;
+    if (g.dim != 2) return fail(ctx, PETTO_INVALID, "write_pgm: only 2D fields");
+    wr::Src src;
+    if (int rc = writer_source(ctx, field, index, &src)) return rc;
+    const int nb = 2 * ctx->nsm;
+    if (!ctx->wmm) CK(cudaMalloc(&ctx->wmm, sizeof(wr::MinMax) * (size_t)nb));
+    wr::MinMax* mm = static_cast<wr::MinMax*>(ctx->wmm);
+    unsigned char* dbytes = nullptr;
+    const size_t nbytes = (size_t)g.nx * g.ny;
+    CK(cudaMalloc(&dbytes, nbytes));
+    wr::k_minmax<<<nb, wr::TB, 0, ctx->stream>>>(src, mm);
+    wr::k_minmax_final<<<1, 32, 0, ctx->stream>>>(mm, nb);
+    wr::k_pgm_bytes<<<blocks_for((long long)nbytes), 256, 0, ctx->stream>>>(src, mm, dbytes);
+    ctx->launches += 3;
+    CKL();
+    std::vector<unsigned char> bytes(nbytes);
+    wr::MinMax h{};
+    CK(cudaMemcpyAsync(bytes.data(), dbytes, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&h, mm, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(dbytes);
+    const bool any = h.ilo != 0x7fffffffffffffffLL;
+    const double lo = any ? h.lo : 0.0, hi = any ? h.hi : 0.0;
+    {
+        OutFile o;
+        if (int rc = open_out(ctx, o, path, true)) return rc;
+        const std::string head = "P5\n" + std::to_string(g.nx) + " " + std::to_string(g.ny) + "\n255\n";
+        std::fwrite(head.data(), 1, head.size(), o.f);
+        std::fwrite(bytes.data(), 1, nbytes, o.f);
+        if (int rc = close_out(ctx, o, path)) return rc;
+    }
+    const std::string side = std::string(path) + ".scale.txt";
+    OutFile o;
+    if (int rc = open_out(ctx, o, side.c_str(), false)) return rc;
+    const std::string body = "min = " + fmt17(lo) + "\nmax = " + fmt17(hi) + "\nrows = top_to_bottom\n";
+    std::fwrite(body.data(), 1, body.size(), o.f);
+    return close_out(ctx, o, side.c_str());
 }
 
 }  // extern "C"

@@ -17,8 +17,19 @@ import numpy as np
 from . import build as _build
 
 MAX_PHASES = 8
-OK, ABORT, INVALID, ERROR = 0, 1, 2, 3
+OK, ABORT, INVALID, ERROR, IO = 0, 1, 2, 3, 4
 MODE_FAST, MODE_REPLICA = 0, 1
+
+
+class IoError(RuntimeError):
+    """The reference's IoError (errors.hpp): a writer could not open or write a file."""
+
+
+FIELD_STATE, FIELD_PHASE, FIELD_PROPERTY = 0, 1, 2
+
+
+class PettoArray(C.Structure):
+    _fields_ = [("field", C.c_int), ("index", C.c_int), ("name", C.c_char_p)]
 
 
 class NumericalAbort(RuntimeError):
@@ -138,6 +149,7 @@ EXPORTED = [
     "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
     "petto_dev_kernel_timing", "petto_dev_kernel_stats", "petto_dev_comm_unique_id", "petto_dev_comm_init",
     "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_peer_export", "petto_dev_peer_import",
+    "petto_dev_write_field_csv", "petto_dev_write_vtk", "petto_dev_write_pgm", "petto_dev_format_values",
 ]
 
 
@@ -228,6 +240,8 @@ class Context:
             raise NumericalAbort(msg, step)
         if rc == INVALID:
             raise ValueError(msg)
+        if rc == IO:
+            raise IoError(msg)
         raise RuntimeError(msg)
 
     def _check(self, rc):
@@ -380,6 +394,28 @@ class Context:
         self._check(lib().petto_dev_peer_import(self.h, lb, hb))
 
     # -- instrumentation -------------------------------------------------------
+    # -- output writers (field_io.cpp) ---------------
+    def write_field_csv(self, field, index, path):
+        self._check(lib().petto_dev_write_field_csv(self.h, field, index, str(path).encode()))
+
+    def write_vtk(self, arrays, path):
+        """arrays: [(field, index, name), ...] in file order."""
+        arr = (PettoArray * len(arrays))(*[PettoArray(f, i, n.encode()) for f, i, n in arrays])
+        self._check(lib().petto_dev_write_vtk(self.h, arr, len(arrays), str(path).encode()))
+
+    def write_pgm(self, field, index, path):
+        self._check(lib().petto_dev_write_pgm(self.h, field, index, str(path).encode()))
+
+    def format_values(self, values, sep_mode=0, row=1):
+        """'%.17g' of every value (host array or device pointer), formatted on the device."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        cap = 25 * len(v) + 1
+        out = C.create_string_buffer(cap)
+        n = C.c_int64()
+        self._check(lib().petto_dev_format_values(self.h, v.ctypes.data_as(C.c_void_p), len(v), sep_mode,
+                                                   max(1, row), out, cap, C.byref(n)))
+        return out.raw[: n.value]
+
     def stream(self):
         return lib().petto_dev_stream(self.h)
 
