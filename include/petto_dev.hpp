@@ -12,17 +12,23 @@
 //   hybrid_solve(hist, op, params)                     dev::hybrid_solve(hist, op, params)
 //   iterate_to_tolerance(hist, op, mode, p, tgt, n)    dev::iterate_to_tolerance(...)
 //   run(prob, sched, cb)                               dev::run(prob, sched, cb)
+//   write_outputs(cfg, prob, result)                   dev::write_outputs(cfg, prob, result)
 //
 // Errors come back as the reference's exception types: NumericalAbort (with the
 // step index), std::invalid_argument, and std::runtime_error for device failures.
 #pragma once
 
+#include <filesystem>
+#include <fstream>
 #include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "petto/engine.hpp"
+#include "petto/errors.hpp"
+#include "petto/field_io.hpp"
 #include "petto/optimizer.hpp"
 #include "petto_dev.h"
 
@@ -39,6 +45,7 @@ inline void check(petto_ctx* ctx, int rc, long long step = -1) {
         throw NumericalAbort(field, step, detail);
     }
     if (rc == PETTO_INVALID) throw std::invalid_argument(msg);
+    if (rc == PETTO_IO) throw IoError(msg);
     throw std::runtime_error(msg);
 }
 
@@ -242,6 +249,111 @@ inline OptimizationResult<double> run(const Problem<double>& prob, const LoopSch
     std::vector<double> prev(result.state.data.size());
     check(c, petto_dev_get_state(c, result.state.data.data(), prev.data()));
     return result;
+}
+
+// write_outputs (engine.cpp:145-217) with the field files formatted on the device
+// (petto_dev_write_field_csv / _pgm / _vtk): the result's phases and state are
+// uploaded once, the property is interpolated on the device, and every field file
+// is byte-identical to the reference's.  history.csv and summary.txt are a few
+// lines of host text, written as the reference writes them.
+inline void write_outputs(const ProblemConfig& cfg, const Problem<double>& prob,
+                          const OptimizationResult<double>& result, int device = 0) {
+    namespace fs = std::filesystem;
+    const fs::path dir(cfg.out_dir);
+    std::error_code ec;
+    fs::create_directories(dir, ec);
+    if (ec) throw IoError("cannot create output directory '" + cfg.out_dir + "'");
+    auto path = [&](const std::string& name) { return (dir / name).string(); };
+    auto wants = [&](const char* f) {
+        for (const std::string& x : cfg.formats)
+            if (x == f) return true;
+        return false;
+    };
+    const Grid& g = *prob.grid;
+    write_history_csv(result.history, path("history.csv"));
+
+    const bool thermal = prob.kind == MaterialKind::Thermal;
+    Context cx(g, thermal ? 0 : 1, prob.material.poisson_ratio, PETTO_MODE_FAST, device);
+    petto_ctx* c = cx.get();
+    petto_material m{};
+    m.kind = thermal ? 0 : 1;
+    m.nphases = result.phases.count();
+    if (m.nphases > PETTO_MAX_PHASES) throw std::invalid_argument("petto_dev: at most 8 phases");
+    for (int i = 0; i < m.nphases; ++i) m.properties[i] = prob.material.properties[i];
+    m.poisson_ratio = prob.material.poisson_ratio;
+    m.penalty = prob.material.penalty;
+    m.void_floor = prob.material.void_floor;
+    petto_targets t{};
+    for (int i = 0; i < m.nphases; ++i) t.fractions[i] = prob.targets.fractions.at(i);
+    const petto_weights w{1.0, 0.0, 0.0, 0.0, 0, -1};
+    check(c, petto_dev_set_design(c, &m, &t, &w));
+    const Index N = g.num_nodes();
+    std::vector<double> buf(static_cast<size_t>(N) * m.nphases);
+    for (int i = 0; i < m.nphases; ++i)
+        std::copy(result.phases.phases[i].data.begin(), result.phases.phases[i].data.end(),
+                  buf.begin() + static_cast<size_t>(i) * N);
+    check(c, petto_dev_set_phases(c, buf.data()));
+    check(c, petto_dev_interpolate(c, nullptr));  // interpolate(result.phases, prob.material)
+    check(c, petto_dev_set_state(c, result.state.data.data(), result.state.data.data()));
+    const char* prop_name = thermal ? "conductivity" : "modulus";
+
+    if (g.dim == 2) {
+        for (int i = 0; i < m.nphases; ++i) {
+            const std::string base = "phase_" + std::to_string(i);
+            if (wants("csv")) check(c, petto_dev_write_field_csv(c, PETTO_FIELD_PHASE, i, path(base + ".csv").c_str()));
+            if (wants("pgm")) check(c, petto_dev_write_pgm(c, PETTO_FIELD_PHASE, i, path(base + ".pgm").c_str()));
+        }
+        const std::string pn(prop_name);
+        if (wants("csv")) check(c, petto_dev_write_field_csv(c, PETTO_FIELD_PROPERTY, 0, path(pn + ".csv").c_str()));
+        if (wants("pgm")) check(c, petto_dev_write_pgm(c, PETTO_FIELD_PROPERTY, 0, path(pn + ".pgm").c_str()));
+        if (thermal) {
+            check(c, petto_dev_write_field_csv(c, PETTO_FIELD_STATE, 0, path("temperature.csv").c_str()));
+        } else {
+            for (int k = 0; k < g.dim; ++k)
+                check(c, petto_dev_write_field_csv(c, PETTO_FIELD_STATE, k,
+                                                   path("displacement_" + component_name(k) + ".csv").c_str()));
+        }
+    } else {
+        std::vector<std::string> names;
+        std::vector<petto_array> arrays;
+        for (int i = 0; i < m.nphases; ++i) names.push_back("phase_" + std::to_string(i));
+        names.push_back(prop_name);
+        for (int k = 0; k < result.state.components; ++k) names.push_back("displacement_" + component_name(k));
+        for (int i = 0; i < m.nphases; ++i) arrays.push_back({PETTO_FIELD_PHASE, i, nullptr});
+        arrays.push_back({PETTO_FIELD_PROPERTY, 0, nullptr});
+        for (int k = 0; k < result.state.components; ++k) arrays.push_back({PETTO_FIELD_STATE, k, nullptr});
+        for (size_t a = 0; a < arrays.size(); ++a) arrays[a].name = names[a].c_str();
+        check(c, petto_dev_write_vtk(c, arrays.data(), static_cast<int>(arrays.size()), path("fields.vtk").c_str()));
+    }
+
+    std::ofstream sum(path("summary.txt"));
+    if (!sum) throw IoError("cannot write run summary");
+    sum << "preset = " << (cfg.preset.empty() ? "(custom)" : cfg.preset) << "\n";
+    sum << "termination = " << to_string(result.termination) << "\n";
+    if (!result.abort_detail.empty()) sum << "abort_detail = " << result.abort_detail << "\n";
+    sum << "loops = " << result.loops << "\n";
+    sum << "apt_steps = " << result.apt_steps << "\n";
+    sum << "pt_steps = " << result.pt_steps << "\n";
+    sum << "design_updates = " << result.design_updates << "\n";
+    sum << "ch_steps = " << result.ch_steps << "\n";
+    sum << "clamp_mass_drift = " << result.clamp_mass_drift << "\n";
+    const LoopSchedule sched = build_schedule(cfg, g);
+    sum << "dt_pt = " << sched.pt.dt_pt << "\n";
+    sum << "dt_apt = " << sched.pt.dt_apt << "\n";
+    sum << "dt_ch = " << sched.ch.dt << "\n";
+    const ObjectiveWeights ew = effective_weights(cfg, g);
+    sum << "alpha_volume_effective = " << ew.alpha_volume << "\n";
+    sum << "alpha_unity_effective = " << ew.alpha_unity << "\n";
+    sum << "alpha_region_effective = " << ew.alpha_region << "\n";
+    if (!result.history.empty()) {
+        const HistoryRecord& r = result.history.back();
+        sum << "final_compliance = " << r.compliance << "\n";
+        sum << "final_r_pde = " << r.r_pde << "\n";
+        sum << "final_separation = " << r.separation << "\n";
+        for (std::size_t i = 0; i < r.volume_fractions.size(); ++i)
+            sum << "final_volfrac_" << i << " = " << r.volume_fractions[i] << "\n";
+        sum << "wall_seconds = " << r.wall_seconds << "\n";
+    }
 }
 
 }  // namespace petto::dev

@@ -6,6 +6,10 @@
 // Prints one line per check and exits non-zero on failure.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <sstream>
 #include <string>
 
@@ -132,6 +136,46 @@ int main() {
             caught = e.step() == 100 && e.field() == "state";
         }
         expect(caught, "dev::hybrid_solve raises NumericalAbort(state, 100)");
+    }
+    // 4. write_outputs: the reference's files and the device writers' files for the
+    //    same result are byte-identical (2D: CSV + PGM per field; 3D: fields.vtk)
+    {
+        namespace fs = std::filesystem;
+        char tmpl[] = "/tmp/petto_dropin_XXXXXX";
+        const fs::path root = mkdtemp(tmpl);
+        auto slurp = [](const fs::path& p) {
+            std::ifstream in(p, std::ios::binary);
+            return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        };
+        const char* cases[] = {
+            "preset = mbb2d\nnx = 40\nny = 16\nproperties = 1, 0.55, 1e-6\ntarget_fractions = 0.2, 0.2, 0.6\n"
+            "max_loops = 2\nn_apt = 20\nn_pt = 20\n",
+            "preset = heat2d\nnx = 33\nny = 29\nmax_loops = 2\nn_apt = 30\nn_pt = 30\n",
+            "preset = cantilever3d\nnx = 20\nny = 9\nnz = 7\nlength_x = 2\nlength_y = 1\nlength_z = 1\n"
+            "properties = 1, 1e-6\ntarget_fractions = 0.3, 0.7\nmax_loops = 2\nn_apt = 20\nn_pt = 20\n"};
+        int k = 0;
+        for (const char* text : cases) {
+            ProblemConfig cfg = cfg_of(text);
+            const Problem<double> prob = build_problem<double>(cfg);
+            const OptimizationResult<double> res = run(prob, build_schedule(cfg, *prob.grid));
+            const fs::path a = root / ("ref" + std::to_string(k)), b = root / ("dev" + std::to_string(k));
+            cfg.out_dir = a.string();
+            write_outputs(cfg, prob, res);
+            cfg.out_dir = b.string();
+            dev::write_outputs(cfg, prob, res);
+            int files = 0, same = 0;
+            for (const auto& e : fs::directory_iterator(a)) {
+                ++files;
+                if (slurp(e.path()) == slurp(b / e.path().filename())) ++same;
+                else std::printf("  differs: %s\n", e.path().filename().c_str());
+            }
+            char buf[160];
+            std::snprintf(buf, sizeof buf, "dev::write_outputs vs write_outputs (%s): %d/%d files identical",
+                          cfg.preset.c_str(), same, files);
+            expect(files > 2 && same == files, buf);
+            ++k;
+        }
+        fs::remove_all(root);
     }
     std::printf("%s\n", failures ? "FAILED" : "ALL PASSED");
     return failures ? 1 : 0;
