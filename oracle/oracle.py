@@ -458,3 +458,11 @@ def ref_config_json(text):
     lib = load("reference").lib
     lib.ref_config_json.restype = C.c_char_p
     return json.loads(lib.ref_config_json(text.encode()).decode())
+
+
+def ref_check_config(text):
+    """Reference-only: parse_config (+ validate_config); None or the ConfigError message."""
+    lib = load("reference").lib
+    lib.orc_last_error.restype = C.c_char_p
+    rc = lib.ref_check_config(text.encode())
+    return None if rc == 0 else lib.orc_last_error().decode()

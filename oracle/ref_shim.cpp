@@ -483,6 +483,14 @@ static std::string num(double v) {
     return buf;
 }
 
+// parse_config + validate_config of a config text: 0, or 3 with the ConfigError message
+int ref_check_config(const char* text) {
+    return guarded([&] {
+        std::istringstream in(text);
+        (void)parse_config(in, "<text>");
+    });
+}
+
 const char* ref_config_json(const char* text) {
     g_json.clear();
     const int rc = guarded([&] {

@@ -234,6 +234,11 @@ class ProblemConfig:
     report_every: int = 10
     initial_phase: float = 0.5
     initial_state: float = 0.0
+    # execution & output (problem_config.hpp:98-102)
+    out_dir: str = ""
+    precision: str = "f64"
+    threads: int = 1
+    formats: List[str] = field(default_factory=lambda: ["csv", "pgm", "vtk"])
 
 
 def _common():
@@ -416,8 +421,12 @@ def parse_config(text: str) -> ProblemConfig:
             c.apt_form = v
         elif k.startswith("roller_") or k.startswith("load_") or k in ("roller_count", "load_count"):
             deferred[k] = v
-        elif k in ("out_dir", "precision", "threads", "formats"):
-            pass
+        elif k in ("out_dir", "precision"):
+            setattr(c, k, v)
+        elif k == "threads":
+            c.threads = int(_parse_double(k, v))
+        elif k == "formats":
+            c.formats = _split_list(v)
         else:
             raise ConfigError(f"line {lineno}: unknown config key '{k}'")
     if "roller_count" in deferred:
@@ -434,6 +443,106 @@ def parse_config(text: str) -> ProblemConfig:
             c.loads.append(LoadSpec(_parse_box(b + "_box", deferred[b + "_box"]), d,
                                     _parse_double(b, deferred[b + "_magnitude"])))
     return c
+
+
+def validate_config(c: ProblemConfig):
+    """validate_config (src/problem_config.cpp:219-299): ConfigError on the first violation."""
+    def fail(fld, constraint):
+        raise ConfigError(f"config field '{fld}': {constraint}")
+
+    def check_box(fld, b, dim):
+        for a in range(dim):
+            if b.lo[a] > b.hi[a]:
+                fail(fld, "box lo must not exceed hi")
+            if b.lo[a] < -1e-9 or b.hi[a] > c.lengths[a] + 1e-9:
+                fail(fld, "box must lie inside the domain")
+
+    dim = 3 if c.nz > 1 else 2
+    if c.nx < 3:
+        fail("nx", "needs at least 3 nodes per axis")
+    if c.ny < 3:
+        fail("ny", "needs at least 3 nodes per axis")
+    if dim == 3 and c.nz < 3:
+        fail("nz", "needs at least 3 nodes per axis (or 1 for 2D)")
+    for a in range(dim):
+        if not c.lengths[a] > 0.0:
+            fail("lengths", "domain extents must be positive")
+    if not c.properties:
+        fail("properties", "at least one phase property required")
+    if any(not p > 0.0 for p in c.properties):
+        fail("properties", "must be positive")
+    if c.penalty < 1.0:
+        fail("penalty", "must be >= 1")
+    if not c.void_floor > 0.0:
+        fail("void_floor", "must be positive")
+    if c.physics == "elasticity" and (c.poisson_ratio <= -1.0 or c.poisson_ratio >= 0.5):
+        fail("poisson_ratio", "must lie in (-1, 0.5)")
+    if len(c.target_fractions) != len(c.properties):
+        fail("target_fractions", "one target per phase required")
+    total = 0.0
+    for t in c.target_fractions:
+        if t < 0.0 or t > 1.0:
+            fail("target_fractions", "each target must lie in [0,1]")
+        total += t
+    if total > 1.0 + 1e-6:
+        fail("target_fractions", "targets must sum to at most 1")
+    if c.has_region:
+        if len(c.region_fractions) != len(c.properties):
+            fail("region_fractions", "one region target per phase required")
+        if any(t < 0.0 or t > 1.0 for t in c.region_fractions):
+            fail("region_fractions", "targets must lie in [0,1]")
+        check_box("region_box", c.region_box, dim)
+    if min(c.alpha_compliance, c.alpha_volume, c.alpha_unity, c.alpha_region) < 0:
+        fail("alpha_*", "weights must be non-negative")
+    if c.alpha_compliance + c.alpha_volume + c.alpha_unity + c.alpha_region <= 0:
+        fail("alpha_*", "at least one weight must be positive")
+    if c.compliance_sign not in (1, -1):
+        fail("compliance_sign", "must be +1 or -1")
+    if c.weight_ref_nodes < 0:
+        fail("weight_ref_nodes", "must be >= 0")
+    if c.n_apt < 0 or c.n_pt < 0 or c.n_apt + c.n_pt < 1:
+        fail("n_apt/n_pt", "need at least one state step per loop")
+    if not c.theta > 0.0:
+        fail("theta", "must be positive")
+    if c.apt_form not in ("explicit", "semi_implicit"):
+        fail("apt_form", "must be 'explicit' or 'semi_implicit'")
+    if not c.ch_mobility > 0.0:
+        fail("ch_mobility", "must be positive")
+    if not c.ch_gamma > 0.0:
+        fail("ch_gamma", "must be positive")
+    if c.dt_pt < 0 or c.dt_apt < 0 or c.dt_ch < 0:
+        fail("dt_*", "must be >= 0 (0 = auto)")
+    if c.dt_ch == 0.0 and not c.dt_ch_multiplier > 0.0:
+        fail("dt_ch_multiplier", "must be positive when dt_ch is auto")
+    if c.max_loops < 1:
+        fail("max_loops", "must be >= 1")
+    if not c.convergence_tol > 0.0:
+        fail("convergence_tol", "must be positive")
+    if c.convergence_window < 2:
+        fail("convergence_window", "must be >= 2")
+    if c.report_every < 1:
+        fail("report_every", "must be >= 1")
+    faces = FACE_NAMES[: 2 * dim]
+    if c.physics == "heat":
+        if any(f not in faces for f in c.dirichlet_faces):
+            fail("dirichlet_faces", "face not in domain")
+    else:
+        if any(f not in faces for f in c.fixed_faces):
+            fail("fixed_faces", "face not in domain")
+        for r in c.rollers:
+            check_box("rollers", r.box, dim)
+            if r.component < 0 or r.component >= dim:
+                fail("rollers", "invalid component")
+        for ld in c.loads:
+            check_box("loads", ld.box, dim)
+            if not sum(d * d for d in ld.direction) > 0.0:
+                fail("loads", "direction must be nonzero")
+    if c.precision not in ("f32", "f64"):
+        fail("precision", "must be 'f32' or 'f64'")
+    if c.threads < 0:
+        fail("threads", "must be >= 0")
+    if c.initial_phase < 0.0 or c.initial_phase > 1.0:
+        fail("initial_phase", "must lie in [0,1]")
 
 
 # --------------------------------------------------------------- assembly
