@@ -121,6 +121,7 @@ struct petto_ctx {
     void* wmm = nullptr;                  // PGM min/max partials
 
     // instrumentation
+    unsigned long long* cta_probe = nullptr;  // probe builds only (E3_CTA_TIMING)
     long long launches = 0;
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;

@@ -101,6 +101,7 @@ struct Params {
     const double* aux; // pinned values / loads (3 x Ns)
     double* partials;  // per-CTA sum of r^2 over unconstrained entries (nullable)
     DeviceStatus* status;
+    unsigned long long* cta_ns;  // probe builds (E3_CTA_TIMING): [grid][2] globaltimer at start / end
     long long step, nsteps;  // 1-based step index within the solve, total steps
     int ntx;           // x tiles of 32 nodes
     int nstrips;       // y strips of W rows
@@ -425,6 +426,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
     if (skip_step(P.status, P.step, P.nsteps)) return;
+#ifdef E3_CTA_TIMING
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
@@ -618,6 +623,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     }
     if (bad && l == 0) mark_bad(P.status, P.step);
     if (w == 0) tmem_dealloc(tbase, TMEM_COLS);
+#ifdef E3_CTA_TIMING
+    if (threadIdx.x == 0 && P.cta_ns) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.cta_ns[3 * blockIdx.x] = t_start;
+        P.cta_ns[3 * blockIdx.x + 1] = t_end;
+        P.cta_ns[3 * blockIdx.x + 2] = smid;
+    }
+#endif
 }
 
 // Cell modulus of every stored cell (i, j, k), k = ks0 + kl: the operator scale

@@ -440,6 +440,14 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
                 }
             }
             P.aux = ctx->aux;
+#ifdef E3_CTA_TIMING
+            {
+                static unsigned long long* probe = nullptr;
+                if (!probe) cudaMalloc(&probe, sizeof(unsigned long long) * 3 * 1024);
+                P.cta_ns = probe;
+                ctx->cta_probe = probe;
+            }
+#endif
             P.partials = partials;
             P.status = ctx->status;
             P.step = step;
@@ -1935,6 +1943,16 @@ double petto_dev_spectral_bound(int dim, const int64_t n[3], const double length
     for (int a = 0; a < dim; ++a) h[a] = length[a] / (double)(n[a] - 1);
     return spectral_bound(dim, h, nu, e_max);
 }
+
+#ifdef E3_CTA_TIMING
+// probe builds only: the last fused launch's per-CTA globaltimer start/end and SM id
+int petto_dev_probe_cta_times(petto_ctx* ctx, uint64_t* out, int n) {
+    if (!ctx->cta_probe) return fail(ctx, PETTO_INVALID, "no fused launch yet");
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->cta_probe, sizeof(uint64_t) * 3 * (size_t)n, cudaMemcpyDeviceToHost));
+    return PETTO_OK;
+}
+#endif
 
 int64_t petto_dev_launch_count(const petto_ctx* ctx) { return ctx->launches; }
 
