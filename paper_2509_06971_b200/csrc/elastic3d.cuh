@@ -478,7 +478,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 for (int q4 = 0; q4 < 4; ++q4)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+#ifndef E3_PROBE_NOPROLOGUE  // probe build (wrong results): no cell work in the prologue
                 cell<false>(P, B0, Bc, sc[0], top, Yd, nullptr);
+#endif
             } else {
                 double* sYw = sY + (q & 1) * (NWARP * YS) + w * YS + l;
                 double B1[4][3], Y0[2][3], Y1[2][3];
@@ -502,7 +504,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 }
             }
             tmem_fence_before();
+#ifdef E3_SLOT_TIMING  // probe: warp 1 of CTA 0 records when it reaches / leaves each barrier
+            unsigned long long t_arrive;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arrive));
+#endif
             __syncthreads();  // task q's shares and sums are complete
+#ifdef E3_SLOT_TIMING
+            if (blockIdx.x == 0 && w == 1 && l == 0 && P.cta_ns && q < 1000) {
+                unsigned long long t_leave;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_leave));
+                P.cta_ns[1024 + 3 * q] = t_arrive;
+                P.cta_ns[1024 + 3 * q + 1] = t_leave;
+                P.cta_ns[1024 + 3 * q + 2] = own ? 1 : 0;
+            }
+#endif
             ++q;
             if (++st == S) {
                 st = 0;

@@ -313,8 +313,9 @@ StepCoef coef(int form, double dt, double theta) {
 void plan_3d(const petto_ctx* ctx, int nstrips, int& chunk, int& nitems, int& grid) {
     // Work items = y-strips x z-chunks of an even length L <= LMAX, one CTA per SM.
     // A CTA's time is (items per CTA) x (x tiles) x (a prologue, ~0.6 of a two-plane
-    // task, + L/2 tasks): pick the L that minimises it (a partial second wave costs
-    // a whole wave; shorter chunks restart the z stream more often).
+    // task -- measured with the slot probe, tools/cta_times.py -- + L/2 tasks): pick
+    // the L that minimises it (a partial second wave costs a whole wave; shorter
+    // chunks restart the z stream more often).
     const int nzo = ctx->g.ke - ctx->g.kb;
     double best = 1e300;
     chunk = 2;
@@ -443,7 +444,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
 #ifdef E3_CTA_TIMING
             {
                 static unsigned long long* probe = nullptr;
-                if (!probe) cudaMalloc(&probe, sizeof(unsigned long long) * 3 * 1024);
+                if (!probe) cudaMalloc(&probe, sizeof(unsigned long long) * 4 * 1024);
                 P.cta_ns = probe;
                 ctx->cta_probe = probe;
             }
@@ -1949,7 +1950,7 @@ double petto_dev_spectral_bound(int dim, const int64_t n[3], const double length
 int petto_dev_probe_cta_times(petto_ctx* ctx, uint64_t* out, int n) {
     if (!ctx->cta_probe) return fail(ctx, PETTO_INVALID, "no fused launch yet");
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->cta_probe, sizeof(uint64_t) * 3 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, ctx->cta_probe, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost));
     return PETTO_OK;
 }
 #endif
