@@ -15,7 +15,10 @@ __global__ void k(double* out, int iters, double a, double b) {
             for (int i = 0; i < ILP; ++i) {
                 if (OP == 0) x[i] = fma(x[i], a, b);
                 else if (OP == 1) x[i] = x[i] + b;
-                else x[i] = x[i] * a;
+                else if (OP == 2) x[i] = x[i] * a;
+                else if (OP == 3) x[i] = x[i] + x[(i + 1) % ILP];           // two vector operands
+                else if (OP == 4) x[i] = fma(x[i], x[(i + 1) % ILP], x[(i + 2) % ILP]);  // three
+                else x[i] = fma(x[i], a, x[(i + 1) % ILP]);                // two + uniform (the kernel's form)
             }
     }
     double s = 0;
@@ -43,7 +46,7 @@ void run(const char* name, int warps_per_sm, int nsm, int clk_mhz) {
     const double winstr = (double)warps_per_sm * iters * 16 * ILP;  // per SM
     const double cycles = ms * 1e-3 * clk_mhz * 1e6;
     printf("%-5s ILP=%d warps/SM=%2d : %.3f warp-instr/clk/SM  (%.2f TFLOP/s-equiv)\n", name, ILP, warps_per_sm,
-           winstr / cycles, winstr * 32 * nsm * (OP == 0 ? 2 : 1) / (ms * 1e-3) / 1e12);
+           winstr / cycles, winstr * 32 * nsm * (OP == 0 || OP >= 4 ? 2 : 1) / (ms * 1e-3) / 1e12);
     cudaFree(out);
 }
 
@@ -56,6 +59,14 @@ int main() {
         run<2, 0>("dfma", w, nsm, clk);
         run<4, 0>("dfma", w, nsm, clk);
         run<8, 0>("dfma", w, nsm, clk);
+    }
+    for (int w : {8, 16}) {
+        run<4, 3>("dadd2", w, nsm, clk);
+        run<8, 3>("dadd2", w, nsm, clk);
+        run<4, 4>("dfma3", w, nsm, clk);
+        run<8, 4>("dfma3", w, nsm, clk);
+        run<4, 5>("dfma2u", w, nsm, clk);
+        run<8, 5>("dfma2u", w, nsm, clk);
     }
     for (int w : {8, 16}) {
         run<1, 1>("dadd", w, nsm, clk);
