@@ -122,6 +122,7 @@ struct petto_ctx {
 
     // instrumentation
     unsigned long long* cta_probe = nullptr;  // probe builds only (E3_CTA_TIMING)
+    bool no_tblock = false;                   // PETTO_NO_TBLOCK=1: per-step grid barriers for 2D heat
     long long launches = 0;
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;

@@ -218,4 +218,156 @@ __global__ void __launch_bounds__(256) k_small_solve(const SolveParams S) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking for small 2D heat grids: the whole hybrid_solve in one
+// cooperative launch, K steps per grid barrier.  A CTA owns a TBX x TBY tile; per
+// round it loads the tile plus a K-node halo of T_n, T_{n-1}, kappa, mask,
+// pinned values and source into shared memory, advances it k <= K steps there
+// (the halo's outer layers go stale one node per step, never reaching the tile),
+// writes the tile's two time levels back, and waits at one grid barrier.  The
+// per-node arithmetic is heat_node + fused_update's (stencil.hpp:123-158,
+// state_solver.hpp:400-442).  Rounds never cross a multiple of 100 steps, so the
+// check_finite abort (state_solver.hpp:463-497) stops exactly where the per-step
+// solve does; global levels alternate between two buffer pairs so no CTA
+// overwrites a tile another CTA is still reading.
+constexpr int TBK = 10;                          // steps per round (divides 100)
+constexpr int TRX = 64, TRY = 32, TRN = TRX * TRY; // shared region: a thread per column, rows ty and ty + 16
+constexpr int TBX = TRX - 2 * TBK, TBY = TRY - 2 * TBK;  // owned tile 44 x 12
+constexpr int TB_THREADS = 1024;
+
+struct TBParams {
+    FusedParams base;
+    double* pair[2][2];   // [pair][0 current, 1 previous]; pair 0 = the caller's (current, previous)
+    long long n_apt, n_pt;
+    int form_apt;
+    double a, b, inv, dt_pt;
+    int tiles_x;
+};
+
+__device__ __forceinline__ double tb_flux(const double* f, const double* kp, int t, int n, int s, double hih2) {
+    const double f0 = f[0], k0 = kp[0];
+    if (t == 0) return (k0 + kp[s]) * (f[s] - f0) * (2.0 * hih2);
+    if (t == n - 1) return (k0 + kp[-s]) * (f[-s] - f0) * (2.0 * hih2);
+    return ((k0 + kp[s]) * (f[s] - f0) - (kp[-s] + k0) * (f0 - f[-s])) * hih2;
+}
+
+__global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    extern __shared__ __align__(16) unsigned char tb_smem[];
+    double* buf[3] = {reinterpret_cast<double*>(tb_smem), reinterpret_cast<double*>(tb_smem) + TRN,
+                      reinterpret_cast<double*>(tb_smem) + 2 * TRN};
+    double* kap = reinterpret_cast<double*>(tb_smem) + 3 * TRN;
+    double* pin = kap + TRN;
+    double* src = pin + TRN;
+    unsigned char* msk = reinterpret_cast<unsigned char*>(src + TRN);
+    const FusedParams& P = S.base;
+    const Geo& g = P.g;
+    const long long nsteps = S.n_apt + S.n_pt;
+    const int x0 = (blockIdx.x % S.tiles_x) * TBX, y0 = (blockIdx.x / S.tiles_x) * TBY;
+    const int rx0 = x0 - TBK, ry0 = y0 - TBK;
+    // this thread: region column lx, rows ly[0], ly[1]
+    const int lx = threadIdx.x & (TRX - 1), gx = rx0 + lx;
+    const int ly[2] = {(int)(threadIdx.x >> 6), (int)(threadIdx.x >> 6) + 16};
+    const bool colin = gx >= 0 && gx < g.nx;
+    bool in[2], own[2];
+    long long node[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int gy = ry0 + ly[h];
+        in[h] = colin && gy >= 0 && gy < g.ny;
+        own[h] = in[h] && lx >= TBK && lx < TBK + TBX && ly[h] >= TBK && ly[h] < TBK + TBY;
+        node[h] = in[h] ? (long long)gy * g.px + gx : 0;
+    }
+    // kappa, mask, pinned values, source: constant through the solve
+    unsigned bad = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int q = ly[h] * TRX + lx;
+        kap[q] = in[h] ? P.prop[node[h]] : 1.0;
+        const unsigned char m = in[h] ? P.mask[node[h]] : 0;
+        msk[q] = m;
+        pin[q] = (m & 1) ? P.aux[node[h]] : 0.0;
+        src[q] = in[h] ? (P.src ? P.src[node[h]] : P.src_uniform) : 0.0;
+        if (own[h] && !(kap[q] > 0.0)) bad |= 2u;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicOr(&P.status->flags, 2u);
+    long long s0 = 0;  // steps completed
+    int rd = 0;        // pair holding the levels at step s0
+    while (s0 < nsteps) {
+        if (skip_step(P.status, s0 + 1, nsteps)) break;  // read after the barrier: the same in every CTA
+        const int k = (int)min((long long)TBK, min(nsteps - s0, 100 - s0 % 100));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = ly[h] * TRX + lx;
+            buf[0][q] = in[h] ? S.pair[rd][0][node[h]] : 0.0;
+            buf[1][q] = in[h] ? S.pair[rd][1][node[h]] : 0.0;
+        }
+        __syncthreads();
+        int ic = 0, ip = 1, in_ = 2;
+        long long first_bad = PETTO_NO_BAD;
+        for (int sub = 1; sub <= k; ++sub) {
+            const long long step = s0 + sub;
+            const int form = step <= S.n_apt ? S.form_apt : 2;
+            const double* T = buf[ic];
+            const double* Tp = buf[ip];
+            double* Tn = buf[in_];
+            // nodes whose dependencies are still fresh: the region shrinks by one per step
+            const bool colok = lx >= sub && lx < TRX - sub;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!in[h] || !colok || ly[h] < sub || ly[h] >= TRY - sub) continue;
+                const int q = ly[h] * TRX + lx;
+                const double acc = tb_flux(T + q, kap + q, gx, g.nx, 1, P.hih2[0]) +
+                                   tb_flux(T + q, kap + q, ry0 + ly[h], g.ny, TRX, P.hih2[1]);
+                const double r = acc + src[q];
+                const double cu = T[q];
+                double nv;
+                if (msk[q] & 1) {
+                    nv = pin[q];
+                } else if (form == 0) {
+                    const double pp = Tp[q];
+                    nv = 2.0 * cu - pp + S.a * r - S.b * (cu - pp);
+                } else if (form == 1) {
+                    const double pp = Tp[q];
+                    nv = (2.0 * cu - pp + S.b * cu + S.a * r) * S.inv;
+                } else {
+                    nv = cu + S.dt_pt * r;
+                }
+                Tn[q] = nv;
+                if (own[h] && !isfinite(nv) && step < first_bad) first_bad = step;
+            }
+            __syncthreads();
+            const int t = ip;  // previous <- current <- next
+            ip = ic;
+            ic = in_;
+            in_ = t;
+        }
+        if (first_bad != PETTO_NO_BAD) mark_bad(P.status, first_bad);
+        // the tile's two levels into the other pair
+        const int wr = rd ^ 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!own[h]) continue;
+            const int q = ly[h] * TRX + lx;
+            S.pair[wr][0][node[h]] = buf[ic][q];
+            S.pair[wr][1][node[h]] = buf[ip][q];
+        }
+        s0 += k;
+        rd = wr;
+        grid.sync();
+    }
+    // the caller's convention (k_small_solve): after s0 steps the current level is
+    // in the caller's buffer (s0 & 1), the previous one in the other
+    const int cur_slot = (int)(s0 & 1);
+    if (rd == 0 && cur_slot == 0) return;  // already in place
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!own[h]) continue;
+        const double c = S.pair[rd][0][node[h]], pv = S.pair[rd][1][node[h]];
+        S.pair[0][cur_slot][node[h]] = c;
+        S.pair[0][cur_slot ^ 1][node[h]] = pv;
+    }
+}
+
 }  // namespace petto_b200

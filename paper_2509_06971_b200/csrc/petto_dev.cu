@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -863,6 +864,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     cudaMemsetAsync(ctx->src, 0, fb * ctx->comps, ctx->stream);
     cudaMemsetAsync(ctx->r, 0, fb * ctx->comps, ctx->stream);
     ctx->npartials = std::max(4 * ctx->nsm, 1024);
+    if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D heat solve
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
         cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
@@ -1231,6 +1233,40 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
     S.inv = ka.inv;
     S.dt_pt = kp.dt;
     const bool heat = ctx->desc.physics == 0;
+    if (heat && ctx->g.dim == 2 && !ctx->no_tblock) {
+        // temporal blocking: TBK steps per grid barrier on shared-memory tiles
+        const Geo& g = ctx->g;
+        const int tx = (g.nx + TBX - 1) / TBX, ty = (g.ny + TBY - 1) / TBY;
+        const size_t smem = (size_t)TRN * (6 * sizeof(double) + 1);
+        CK(cudaFuncSetAttribute(k_heat2d_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_heat2d_tb, TB_THREADS, smem));
+        if ((long long)tx * ty <= (long long)per_sm * ctx->nsm) {
+            TBParams T{};
+            T.base = S.base;
+            T.pair[0][0] = S.st[0];
+            T.pair[0][1] = S.st[1];
+            T.pair[1][0] = ctx->st[3 - ctx->cur - ctx->prev];  // the spare state buffer
+            T.pair[1][1] = ctx->r;
+            T.n_apt = n_apt;
+            T.n_pt = n_pt;
+            T.form_apt = ka.form;
+            T.a = ka.a;
+            T.b = ka.b;
+            T.inv = ka.inv;
+            T.dt_pt = kp.dt;
+            T.tiles_x = tx;
+            void* targs[] = {&T};
+            cudaEvent_t ev[2];
+            timing_begin(ctx, ev);
+            CK(cudaLaunchCooperativeKernel((const void*)k_heat2d_tb, dim3(tx * ty), dim3(TB_THREADS), targs, smem,
+                                           ctx->stream));
+            timing_end(ctx, ev, "k_heat2d_tb", (double)owned_nodes(ctx) * 33.0 * (double)(n_apt + n_pt));
+            ctx->launches++;
+            CKL();
+            return PETTO_OK;
+        }
+    }
     const void* fn = heat ? (const void*)k_small_solve<0> : (const void*)k_small_solve<1>;
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
