@@ -276,3 +276,62 @@ def test_elasticity3d_reckless_abort_step(n_apt):
         steps.append(ei.value.step)
     assert steps[0] == steps[1]
     assert steps[0] % 100 == 0 or steps[0] == n_apt
+
+
+def _heat_ctx_solve(g, kappa, src, bc, T0, p, tblock):
+    """hybrid_solve of a 2D heat problem with or without temporal blocking (PETTO_NO_TBLOCK)."""
+    import os
+
+    old = os.environ.get("PETTO_NO_TBLOCK")
+    os.environ["PETTO_NO_TBLOCK"] = "0" if tblock else "1"
+    try:
+        op = D.HeatOperator(g, kappa, src, bc, mode=FAST)
+    finally:
+        if old is None:
+            del os.environ["PETTO_NO_TBLOCK"]
+        else:
+            os.environ["PETTO_NO_TBLOCK"] = old
+    hist = D.StateHistory(T0.copy(), T0.copy())
+    step = None
+    try:
+        D.hybrid_solve(hist, op, p)
+    except D.NumericalAbort as e:
+        step = e.step
+    return hist, step
+
+
+def test_heat2d_temporal_blocking_matches_per_step_solve(port):
+    """The temporally blocked 2D heat solve (10 steps per grid barrier, shared-memory
+    tiles with halo) against the per-step solve and the oracle: many tiles, ragged
+    edges, a dense source, pinned faces, and rounds that straddle the APT -> PT switch."""
+    g = P.Grid.make2d(203, 151, 2.0, 1.5)
+    bc = P.BoundarySpec.all_faces(2, P.NEUMANN_ZERO)
+    bc.face[0] = P.FaceCondition(P.DIRICHLET, 0.25, 0)
+    bc.face[3] = P.FaceCondition(P.DIRICHLET, -0.5, 0)
+    r = H.rng(5)
+    kappa = np.maximum(1e-3, r.random(g.num_nodes) ** 2)
+    src = r.uniform(-1.0, 1.0, g.num_nodes)
+    T0 = r.uniform(-0.1, 0.1, g.num_nodes)
+    e, v = P.make_constraints(g, bc, 1)
+    T0[e] = v
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=137, n_pt=63, form=1)
+    a, _ = _heat_ctx_solve(g, kappa, src, bc, T0, p, True)
+    b, _ = _heat_ctx_solve(g, kappa, src, bc, T0, p, False)
+    assert rel_err(a.current, b.current) < 1e-13 and rel_err(a.previous, b.previous) < 1e-13
+    rc, wc, wp, _ = port.hybrid_solve(0, g, bc, kappa, 0.3, src, T0, T0, p)
+    assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
+
+
+def test_heat2d_temporal_blocking_abort_state():
+    """An exploding 2D heat solve aborts at the same check_finite step with the same
+    buffers (the state of that step) in the blocked and the per-step solve."""
+    g = P.Grid.make2d(90, 70, 1.0, 1.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    T0 = H.rng(6).uniform(-1e-3, 1e-3, g.num_nodes)
+    p = P.PTParams(dt_pt=5e-4, dt_apt=0.5 / 15, theta=1.0, n_apt=0, n_pt=5000)
+    a, sa = _heat_ctx_solve(g, np.ones(g.num_nodes), np.ones(g.num_nodes), bc, T0, p, True)
+    b, sb = _heat_ctx_solve(g, np.ones(g.num_nodes), np.ones(g.num_nodes), bc, T0, p, False)
+    assert sa is not None and sa == sb and sa % 100 == 0
+    same = (a.current == b.current) | (np.isnan(a.current) & np.isnan(b.current))
+    assert same.all()
