@@ -174,7 +174,7 @@ def cpu_baseline(name, prob, sched, E, steps, kind_pref="reference"):
         orc, kind, cores = O.load("port"), "port", 1
     g = prob.grid
     p = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, steps, 0, sched.pt.form)
-    sec = orc.time_hybrid(1, g, prob.bc, E, prob.poisson_ratio, prob.source, prob.initial_state,
+    sec = orc.time_hybrid(prob.physics, g, prob.bc, E, prob.poisson_ratio, prob.source, prob.initial_state,
                           prob.initial_state, p)
     value = g.num_nodes * steps / sec / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
