@@ -46,7 +46,7 @@ def args_():
     a.add_argument("--n-apt", type=int, default=100)
     a.add_argument("--no-e2e", action="store_true")
     a.add_argument("--no-kernel-timing", action="store_true",
-                   help="no per-launch events in the timed region (roofline.achieved then uses the step time)")
+                   help="no launch-duration events (roofline.achieved then uses the step time)")
     a.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                    help="slab ghost planes: stored by the fused kernel into the neighbours (peer) or NCCL send/recv")
     a.add_argument("--e2e-pipeline", type=int, default=3,
@@ -271,8 +271,12 @@ def run_ours(a):
     for _ in range(a.warmup):
         ctx.hybrid_solve(params)
     torch.cuda.synchronize()
+    # timed region: exactly K steps between a barrier + synchronize on both sides.
+    # CUDA events sample every 10th fused launch inside it (roofline.achieved's
+    # launch duration); events around every launch would add ~0.6% to a C5 step
+    # (a third to a C4 step) and drain their pool with host syncs.
     launches0 = ctx.launch_count()
-    ctx.kernel_timing(not a.no_kernel_timing)
+    ctx.kernel_timing(not a.no_kernel_timing, stride=10)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if world > 1:

@@ -282,6 +282,8 @@ int petto_dev_format_values(petto_ctx* ctx, const double* values, int64_t n, int
                             char* out, int64_t cap, int64_t* len);
 
 int64_t petto_dev_launch_count(const petto_ctx* ctx);
+/* Instrumentation: CUDA events around the hot launches (0 off; n >= 1: around
+ * every n-th launch, so a timed region can sample launch durations cheaply). */
 int petto_dev_kernel_timing(petto_ctx* ctx, int enable);
 int petto_dev_kernel_stats(petto_ctx* ctx, double* total_ms, int64_t* launches,
                            double* bytes_per_launch, char* name, int name_cap);

@@ -125,6 +125,8 @@ struct petto_ctx {
     bool no_tblock = false;                   // PETTO_NO_TBLOCK=1: per-step grid barriers for 2D heat
     long long launches = 0;
     bool timing = false;
+    int timing_stride = 1;      // events around every timing_stride-th timed launch
+    long long timing_seq = 0;
     std::vector<cudaEvent_t> ev_pool;
     int ev_used = 0;
     double kernel_ms = 0.0;

@@ -334,7 +334,9 @@ void plan_3d(const petto_ctx* ctx, int nstrips, int& chunk, int& nitems, int& gr
 }
 
 void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
+    ev[0] = ev[1] = nullptr;
     if (!ctx->timing) return;
+    if (ctx->timing_seq++ % ctx->timing_stride) return;  // sample every timing_stride-th launch
     if (ctx->ev_used + 2 > (int)ctx->ev_pool.size()) {
         // drain the pool
         cudaStreamSynchronize(ctx->stream);
@@ -352,7 +354,7 @@ void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
 }
 
 void timing_end(petto_ctx* ctx, cudaEvent_t* ev, const char* name, double bytes) {
-    if (!ctx->timing) return;
+    if (!ctx->timing || !ev[0]) return;
     cudaEventRecord(ev[1], ctx->stream);
     ctx->kernel_launches += 1;
     ctx->bytes_per_launch = bytes;
@@ -2000,6 +2002,8 @@ int petto_dev_kernel_timing(petto_ctx* ctx, int enable) {
         for (auto& e : ctx->ev_pool) CK(cudaEventCreate(&e));
     }
     ctx->timing = enable != 0;
+    ctx->timing_stride = enable > 1 ? enable : 1;
+    ctx->timing_seq = 0;
     ctx->kernel_ms = 0.0;
     ctx->kernel_launches = 0;
     ctx->ev_used = 0;

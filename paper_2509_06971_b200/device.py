@@ -422,8 +422,9 @@ class Context:
     def launch_count(self):
         return lib().petto_dev_launch_count(self.h)
 
-    def kernel_timing(self, enable=True):
-        self._check(lib().petto_dev_kernel_timing(self.h, 1 if enable else 0))
+    def kernel_timing(self, enable=True, stride=1):
+        """CUDA events around every `stride`-th hot launch (kernel_stats averages them)."""
+        self._check(lib().petto_dev_kernel_timing(self.h, max(1, int(stride)) if enable else 0))
 
     def kernel_stats(self):
         ms, n, b = C.c_double(), C.c_int64(), C.c_double()
