@@ -86,6 +86,7 @@ CASES = {
     "cantilever3d": "preset = cantilever3d\nnx = 20\nny = 9\nnz = 7\nlength_x = 2\nlength_y = 1\nlength_z = 1\n"
                     "properties = 1, 1e-6\ntarget_fractions = 0.3, 0.7\nmax_loops = 3\nreport_every = 1\n"
                     "n_apt = 20\nn_pt = 20\n",
+    "drone3d": "preset = drone3d\nnx = 24\nny = 12\nnz = 24\nmax_loops = 3\nreport_every = 1\nn_apt = 20\nn_pt = 20\n",
 }
 FILES = {
     "heat2d": {"history.csv", "summary.txt", "phase_0.csv", "phase_0.pgm", "phase_0.pgm.scale.txt", "phase_1.csv",
@@ -94,6 +95,7 @@ FILES = {
     "mbb2d": {"history.csv", "summary.txt"} | {f"phase_{i}.{e}" for i in range(3) for e in ("csv", "pgm", "pgm.scale.txt")}
              | {"modulus.csv", "modulus.pgm", "modulus.pgm.scale.txt", "displacement_x.csv", "displacement_y.csv"},
     "cantilever3d": {"history.csv", "summary.txt", "fields.vtk"},
+    "drone3d": {"history.csv", "summary.txt", "fields.vtk"},
 }
 
 
@@ -150,9 +152,11 @@ def test_cli_run_against_oracle(port, tmp_path, name, mode):
             assert np.abs(_csv_values(out / f"phase_{i}.csv") - phases[i * N:(i + 1) * N]).max() <= ftol
     else:
         arr = _vtk_arrays(out / "fields.vtk")
-        assert list(arr) == ["phase_0", "phase_1", "modulus", "displacement_x", "displacement_y", "displacement_z"]
+        prop = "modulus" if prob.physics else "conductivity"
+        comps = ["displacement_" + "xyz"[c] for c in range(prob.comps)]  # engine.cpp:183-185, heat too
+        assert list(arr) == [f"phase_{i}" for i in range(prob.nphases)] + [prop] + comps
         for i in range(prob.nphases):
             assert np.abs(arr[f"phase_{i}"] - phases[i * N:(i + 1) * N]).max() <= ftol
-        for c in range(3):
+        for c in range(prob.comps):
             u = state[c * N:(c + 1) * N]
-            assert np.abs(arr["displacement_" + "xyz"[c]] - u).max() <= ftol * max(1.0, np.abs(u).max())
+            assert np.abs(arr[comps[c]] - u).max() <= ftol * max(1.0, np.abs(u).max())
