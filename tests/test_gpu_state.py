@@ -300,10 +300,12 @@ def _heat_ctx_solve(g, kappa, src, bc, T0, p, tblock):
     return hist, step
 
 
-def test_heat2d_temporal_blocking_matches_per_step_solve(port):
+@pytest.mark.parametrize("form,n_apt,n_pt", [(1, 137, 63), (0, 95, 0), (0, 0, 110)])
+def test_heat2d_temporal_blocking_matches_per_step_solve(port, form, n_apt, n_pt):
     """The temporally blocked 2D heat solve (10 steps per grid barrier, shared-memory
     tiles with halo) against the per-step solve and the oracle: many tiles, ragged
-    edges, a dense source, pinned faces, and rounds that straddle the APT -> PT switch."""
+    edges, a dense source, pinned faces, both APT forms, pure PT, and rounds that
+    straddle the APT -> PT switch or end short of 10 steps."""
     g = P.Grid.make2d(203, 151, 2.0, 1.5)
     bc = P.BoundarySpec.all_faces(2, P.NEUMANN_ZERO)
     bc.face[0] = P.FaceCondition(P.DIRICHLET, 0.25, 0)
@@ -315,7 +317,7 @@ def test_heat2d_temporal_blocking_matches_per_step_solve(port):
     e, v = P.make_constraints(g, bc, 1)
     T0[e] = v
     h = g.min_spacing()
-    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=137, n_pt=63, form=1)
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=n_apt, n_pt=n_pt, form=form)
     a, _ = _heat_ctx_solve(g, kappa, src, bc, T0, p, True)
     b, _ = _heat_ctx_solve(g, kappa, src, bc, T0, p, False)
     assert rel_err(a.current, b.current) < 1e-13 and rel_err(a.previous, b.previous) < 1e-13
