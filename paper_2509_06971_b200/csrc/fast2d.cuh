@@ -292,6 +292,32 @@ __global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && (threadIdx.x & 31) == 0) atomicOr(&P.status->flags, 2u);
+    __syncthreads();
+    // per node: the two face sums of each axis, (k0 + k+) and (k- + k0) as the
+    // reference adds them (stencil.hpp:123-158), and the source / pinned value --
+    // constant through the solve, so held in registers (shared memory then only
+    // serves the temperature levels)
+    double cxp[2], cxm[2], cyp[2], cym[2], sr[2], pv[2];
+    int ex[2], ey[2];  // 0 interior, 1 at the low end, 2 at the high end
+    bool pinned[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int q = ly[h] * TRX + lx;
+        const int gy = ry0 + ly[h];
+        const bool interior = lx > 0 && lx < TRX - 1 && ly[h] > 0 && ly[h] < TRY - 1;
+        const double k0 = kap[q];
+        ex[h] = gx == 0 ? 1 : (gx == g.nx - 1 ? 2 : 0);
+        ey[h] = gy == 0 ? 1 : (gy == g.ny - 1 ? 2 : 0);
+        cxp[h] = interior ? k0 + kap[q + 1] : 0.0;
+        cxm[h] = interior ? kap[q - 1] + k0 : 0.0;
+        cyp[h] = interior ? k0 + kap[q + TRX] : 0.0;
+        cym[h] = interior ? kap[q - TRX] + k0 : 0.0;
+        if (ex[h] == 2) cxp[h] = interior ? k0 + kap[q - 1] : 0.0;  // the one neighbour at the high end
+        if (ey[h] == 2) cyp[h] = interior ? k0 + kap[q - TRX] : 0.0;
+        sr[h] = src[q];
+        pinned[h] = msk[q] & 1;
+        pv[h] = pin[q];
+    }
     long long s0 = 0;  // steps completed
     int rd = 0;        // pair holding the levels at step s0
     while (s0 < nsteps) {
@@ -318,13 +344,20 @@ __global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
             for (int h = 0; h < 2; ++h) {
                 if (!in[h] || !colok || ly[h] < sub || ly[h] >= TRY - sub) continue;
                 const int q = ly[h] * TRX + lx;
-                const double acc = tb_flux(T + q, kap + q, gx, g.nx, 1, P.hih2[0]) +
-                                   tb_flux(T + q, kap + q, ry0 + ly[h], g.ny, TRX, P.hih2[1]);
-                const double r = acc + src[q];
-                const double cu = T[q];
+                const double f0 = T[q];
+                double fx, fy;  // flux_fast / tb_flux with the face sums from registers
+                if (ex[h] == 0) fx = (cxp[h] * (T[q + 1] - f0) - cxm[h] * (f0 - T[q - 1])) * P.hih2[0];
+                else if (ex[h] == 1) fx = cxp[h] * (T[q + 1] - f0) * (2.0 * P.hih2[0]);
+                else fx = cxp[h] * (T[q - 1] - f0) * (2.0 * P.hih2[0]);
+                if (ey[h] == 0) fy = (cyp[h] * (T[q + TRX] - f0) - cym[h] * (f0 - T[q - TRX])) * P.hih2[1];
+                else if (ey[h] == 1) fy = cyp[h] * (T[q + TRX] - f0) * (2.0 * P.hih2[1]);
+                else fy = cyp[h] * (T[q - TRX] - f0) * (2.0 * P.hih2[1]);
+                const double acc = fx + fy;
+                const double r = acc + sr[h];
+                const double cu = f0;
                 double nv;
-                if (msk[q] & 1) {
-                    nv = pin[q];
+                if (pinned[h]) {
+                    nv = pv[h];
                 } else if (form == 0) {
                     const double pp = Tp[q];
                     nv = 2.0 * cu - pp + S.a * r - S.b * (cu - pp);
