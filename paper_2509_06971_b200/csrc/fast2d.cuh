@@ -403,4 +403,207 @@ __global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking for small 2D elasticity grids (plane strain): the same scheme
+// as k_heat2d_tb -- EK steps per grid barrier on a shared-memory region with an
+// EK-node halo -- with elastic2d_node's arithmetic per node (the four cells
+// around it in the modal basis, state_solver.hpp:327-385 via stiffness.hpp).
+// Shared memory holds the three displacement levels, the cell moduli (corner sum
+// x scale, once per solve), the pinned values / loads and the mask; 512 threads,
+// each a column of four consecutive region rows.
+constexpr int EK = 4;                              // steps per round (divides 100)
+constexpr int ERX = 64, ERY = 32, ERN = ERX * ERY;
+constexpr int ETX = ERX - 2 * EK, ETY = ERY - 2 * EK;  // owned tile 56 x 24
+constexpr int ETHREADS = 512, EROWS = ERY / (ETHREADS / ERX);  // 4 rows per thread
+constexpr size_t E_SMEM = (size_t)ERN * (sizeof(double) * (3 * 2 + 1 + 2) + 1);
+
+__global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    extern __shared__ __align__(16) unsigned char tb_smem[];
+    double* U = reinterpret_cast<double*>(tb_smem);  // [3 levels][2 comps][ERN]
+    double* EC = U + 6 * ERN;                        // cell whose low corner is the node
+    double* AX = EC + ERN;                           // [2][ERN] pinned value / load
+    unsigned char* MK = reinterpret_cast<unsigned char*>(AX + 2 * ERN);
+    const FusedParams& P = S.base;
+    const Geo& g = P.g;
+    const double* kh = P.kh;
+    const long long nsteps = S.n_apt + S.n_pt;
+    const int x0 = (blockIdx.x % S.tiles_x) * ETX, y0 = (blockIdx.x / S.tiles_x) * ETY;
+    const int rx0 = x0 - EK, ry0 = y0 - EK;
+    const int lx = threadIdx.x & (ERX - 1), gx = rx0 + lx;
+    const int ly0 = (threadIdx.x / ERX) * EROWS;  // rows ly0 .. ly0 + EROWS - 1
+    const bool colin = gx >= 0 && gx < g.nx;
+    bool in[EROWS], own[EROWS];
+    long long node[EROWS];
+    double invv[EROWS];
+#pragma unroll
+    for (int h = 0; h < EROWS; ++h) {
+        const int ly = ly0 + h, gy = ry0 + ly;
+        in[h] = colin && gy >= 0 && gy < g.ny;
+        own[h] = in[h] && lx >= EK && lx < EK + ETX && ly >= EK && ly < EK + ETY;
+        node[h] = in[h] ? (long long)gy * g.px + gx : 0;
+        invv[h] = in[h] ? inv_volume_fast(g, P.inv_base, gx, gy, 0) : 0.0;
+        const int q = ly * ERX + lx;
+        const bool cell = gx >= 0 && gy >= 0 && gx <= g.nx - 2 && gy <= g.ny - 2;
+        if (cell) {
+            const long long b = (long long)gy * g.px + gx;
+            EC[q] = ((P.prop[b] + P.prop[b + 1]) + (P.prop[b + g.px] + P.prop[b + g.px + 1])) * P.e_scale;
+        } else {
+            EC[q] = 0.0;
+        }
+        const unsigned char m = in[h] ? P.mask[node[h]] : 0;
+        MK[q] = m;
+        AX[q] = m ? P.aux[node[h]] : 0.0;
+        AX[ERN + q] = m ? P.aux[g.Ns + node[h]] : 0.0;
+    }
+    long long s0 = 0;
+    int rd = 0;
+    while (s0 < nsteps) {
+        if (skip_step(P.status, s0 + 1, nsteps)) break;  // read after the barrier: the same in every CTA
+        const int k = (int)min((long long)EK, min(nsteps - s0, 100 - s0 % 100));
+#pragma unroll
+        for (int h = 0; h < EROWS; ++h) {
+            const int q = (ly0 + h) * ERX + lx;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                U[(0 * 2 + c) * ERN + q] = in[h] ? S.pair[rd][0][c * g.Ns + node[h]] : 0.0;
+                U[(1 * 2 + c) * ERN + q] = in[h] ? S.pair[rd][1][c * g.Ns + node[h]] : 0.0;
+            }
+        }
+        __syncthreads();
+        int ic = 0, ip = 1, in_ = 2;
+        long long first_bad = PETTO_NO_BAD;
+        for (int sub = 1; sub <= k; ++sub) {
+            const long long step = s0 + sub;
+            const int form = step <= S.n_apt ? S.form_apt : 2;
+            const double* Ux = U + (ic * 2) * ERN;
+            const double* Uy = Ux + ERN;
+            // Column-of-cells sweep: this thread's four nodes (lx, ly0..ly0+3) touch
+            // the cells of columns lx-1, lx in rows ly0-1..ly0+3; each cell is evaluated
+            // once and its corner forces go to the (up to) two nodes of this column
+            // it touches.  Rows run top-down and the x+ cell first, so every node
+            // sums its cells in elastic2d_node's order (m = 0, 1, 2, 3).
+            if (lx >= sub && lx < ERX - sub) {
+                double acc[EROWS][2];
+#pragma unroll
+                for (int h = 0; h < EROWS; ++h) acc[h][0] = acc[h][1] = 0.0;
+                double hi[3][2], lo[3][2];  // rows lcj + 1 and lcj at columns lx-1, lx, lx+1
+                {
+                    const int row = min(ly0 + EROWS, ERY - 1);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        hi[d][0] = Ux[row * ERX + lx - 1 + d];
+                        hi[d][1] = Uy[row * ERX + lx - 1 + d];
+                    }
+                }
+#pragma unroll
+                for (int cr = EROWS; cr >= 0; --cr) {
+                    const int lcj = ly0 - 1 + cr;
+                    const int row = max(lcj, 0);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        lo[d][0] = Ux[row * ERX + lx - 1 + d];
+                        lo[d][1] = Uy[row * ERX + lx - 1 + d];
+                    }
+                    const int gcj = ry0 + lcj;
+                    const bool row_ok = lcj >= sub - 1 && lcj + 1 <= ERY - sub && gcj >= 0 && gcj <= g.ny - 2;
+#pragma unroll
+                    for (int cc = 1; cc >= 0; --cc) {
+                        const int gci = gx - 1 + cc;
+                        if (!row_ok || gci < 0 || gci > g.nx - 2) continue;
+                        double C[4][2];
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            const double v0 = lo[cc][c], v1 = lo[cc + 1][c], v2 = hi[cc][c], v3 = hi[cc + 1][c];
+                            C[1][c] = (v0 - v1) + (v2 - v3);
+                            C[2][c] = (v0 + v1) - (v2 + v3);
+                            C[3][c] = (v0 - v1) - (v2 - v3);
+                        }
+                        const double ec = EC[row * ERX + lx - 1 + cc];
+                        const double F10 = ec * (kh[0] * C[1][0] + kh[1] * C[2][1]);
+                        const double F11 = ec * (kh[2] * C[1][1] + kh[3] * C[2][0]);
+                        const double F20 = ec * (kh[4] * C[1][1] + kh[5] * C[2][0]);
+                        const double F21 = ec * (kh[6] * C[1][0] + kh[7] * C[2][1]);
+                        const double F30 = ec * (kh[8] * C[3][0]);
+                        const double F31 = ec * (kh[9] * C[3][1]);
+                        const double s1 = cc ? 1.0 : -1.0;  // m & 1 = 1 - cc
+                        if (cr >= 1) {  // node row lcj: corner m = 1 - cc
+                            acc[cr - 1][0] += s1 * F10 + 1.0 * F20 + s1 * F30;
+                            acc[cr - 1][1] += s1 * F11 + 1.0 * F21 + s1 * F31;
+                        }
+                        if (cr < EROWS) {  // node row lcj + 1: corner m = (1 - cc) | 2
+                            acc[cr][0] += s1 * F10 + -1.0 * F20 + -s1 * F30;
+                            acc[cr][1] += s1 * F11 + -1.0 * F21 + -s1 * F31;
+                        }
+                    }
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) hi[d][0] = lo[d][0], hi[d][1] = lo[d][1];
+                }
+#pragma unroll
+                for (int h = 0; h < EROWS; ++h) {
+                    const int ly = ly0 + h;
+                    if (!in[h] || ly < sub || ly >= ERY - sub) continue;
+                    const int q = ly * ERX + lx;
+                    const unsigned char mk = MK[q];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const double cu = U[(ic * 2 + c) * ERN + q];
+                        double nv;
+                        if ((mk >> c) & 1) {
+                            nv = AX[c * ERN + q];
+                        } else {
+                            const double f = (mk & 8) ? AX[c * ERN + q] : 0.0;
+                            const double r = -acc[h][c] * invv[h] - f;
+                            if (form == 0) {
+                                const double pp = U[(ip * 2 + c) * ERN + q];
+                                nv = 2.0 * cu - pp + S.a * r - S.b * (cu - pp);
+                            } else if (form == 1) {
+                                const double pp = U[(ip * 2 + c) * ERN + q];
+                                nv = (2.0 * cu - pp + S.b * cu + S.a * r) * S.inv;
+                            } else {
+                                nv = cu + S.dt_pt * r;
+                            }
+                        }
+                        U[(in_ * 2 + c) * ERN + q] = nv;
+                        if (own[h] && !isfinite(nv) && step < first_bad) first_bad = step;
+                    }
+                }
+            }
+            __syncthreads();
+            const int t = ip;
+            ip = ic;
+            ic = in_;
+            in_ = t;
+        }
+        if (first_bad != PETTO_NO_BAD) mark_bad(P.status, first_bad);
+        const int wr = rd ^ 1;
+#pragma unroll
+        for (int h = 0; h < EROWS; ++h) {
+            if (!own[h]) continue;
+            const int q = (ly0 + h) * ERX + lx;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                S.pair[wr][0][c * g.Ns + node[h]] = U[(ic * 2 + c) * ERN + q];
+                S.pair[wr][1][c * g.Ns + node[h]] = U[(ip * 2 + c) * ERN + q];
+            }
+        }
+        s0 += k;
+        rd = wr;
+        grid.sync();
+    }
+    const int cur_slot = (int)(s0 & 1);
+    if (rd == 0 && cur_slot == 0) return;
+#pragma unroll
+    for (int h = 0; h < EROWS; ++h) {
+        if (!own[h]) continue;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const long long e = c * g.Ns + node[h];
+            const double cv = S.pair[rd][0][e], pv = S.pair[rd][1][e];
+            S.pair[0][cur_slot][e] = cv;
+            S.pair[0][cur_slot ^ 1][e] = pv;
+        }
+    }
+}
+
 }  // namespace petto_b200

@@ -866,7 +866,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     cudaMemsetAsync(ctx->src, 0, fb * ctx->comps, ctx->stream);
     cudaMemsetAsync(ctx->r, 0, fb * ctx->comps, ctx->stream);
     ctx->npartials = std::max(4 * ctx->nsm, 1024);
-    if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D heat solve
+    if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D solves
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
         cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
@@ -1235,14 +1235,17 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
     S.inv = ka.inv;
     S.dt_pt = kp.dt;
     const bool heat = ctx->desc.physics == 0;
-    if (heat && ctx->g.dim == 2 && !ctx->no_tblock) {
-        // temporal blocking: TBK steps per grid barrier on shared-memory tiles
+    if (ctx->g.dim == 2 && !ctx->no_tblock) {
+        // temporal blocking: TBK (heat) / EK (elasticity) steps per grid barrier on
+        // shared-memory tiles
         const Geo& g = ctx->g;
-        const int tx = (g.nx + TBX - 1) / TBX, ty = (g.ny + TBY - 1) / TBY;
-        const size_t smem = (size_t)TRN * (6 * sizeof(double) + 1);
-        CK(cudaFuncSetAttribute(k_heat2d_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const void* tfn = heat ? (const void*)k_heat2d_tb : (const void*)k_elastic2d_tb;
+        const int tiw = heat ? TBX : ETX, tih = heat ? TBY : ETY, nthr = heat ? TB_THREADS : ETHREADS;
+        const int tx = (g.nx + tiw - 1) / tiw, ty = (g.ny + tih - 1) / tih;
+        const size_t smem = heat ? (size_t)TRN * (6 * sizeof(double) + 1) : E_SMEM;
+        CK(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_heat2d_tb, TB_THREADS, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tfn, nthr, smem));
         if ((long long)tx * ty <= (long long)per_sm * ctx->nsm) {
             TBParams T{};
             T.base = S.base;
@@ -1261,9 +1264,9 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
             void* targs[] = {&T};
             cudaEvent_t ev[2];
             timing_begin(ctx, ev);
-            CK(cudaLaunchCooperativeKernel((const void*)k_heat2d_tb, dim3(tx * ty), dim3(TB_THREADS), targs, smem,
-                                           ctx->stream));
-            timing_end(ctx, ev, "k_heat2d_tb", (double)owned_nodes(ctx) * 33.0 * (double)(n_apt + n_pt));
+            CK(cudaLaunchCooperativeKernel(tfn, dim3(tx * ty), dim3(nthr), targs, smem, ctx->stream));
+            timing_end(ctx, ev, heat ? "k_heat2d_tb" : "k_elastic2d_tb",
+                       (double)owned_nodes(ctx) * (heat ? 33.0 : 57.0) * (double)(n_apt + n_pt));
             ctx->launches++;
             CKL();
             return PETTO_OK;

@@ -337,3 +337,66 @@ def test_heat2d_temporal_blocking_abort_state():
     assert sa is not None and sa == sb and sa % 100 == 0
     same = (a.current == b.current) | (np.isnan(a.current) & np.isnan(b.current))
     assert same.all()
+
+
+def _elastic2d_ctx_solve(g, E, f, bc, u0, p, tblock):
+    """hybrid_solve of a 2D elasticity problem with or without temporal blocking."""
+    import os
+
+    old = os.environ.get("PETTO_NO_TBLOCK")
+    os.environ["PETTO_NO_TBLOCK"] = "0" if tblock else "1"
+    try:
+        op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=FAST)
+    finally:
+        if old is None:
+            del os.environ["PETTO_NO_TBLOCK"]
+        else:
+            os.environ["PETTO_NO_TBLOCK"] = old
+    hist = D.StateHistory(u0.copy(), u0.copy())
+    step = None
+    try:
+        D.hybrid_solve(hist, op, p)
+    except D.NumericalAbort as e:
+        step = e.step
+    return hist, step
+
+
+@pytest.mark.parametrize("form,n_apt,n_pt", [(1, 137, 63), (0, 95, 0), (0, 0, 110), (1, 3, 2)])
+def test_elastic2d_temporal_blocking_matches_per_step_solve(port, form, n_apt, n_pt):
+    """The temporally blocked 2D elasticity solve (4 steps per grid barrier, 56 x 24
+    tiles with a 4-node halo) against the per-step solve and the oracle: many tiles,
+    ragged edges, a random modulus, point loads, a clamped face plus single-component
+    pins, both APT forms, pure PT, rounds straddling the APT -> PT switch."""
+    g = P.Grid.make2d(203, 77, 2.0, 0.8)
+    E = H.random_modulus(g, 8)
+    f = H.sparse_loads(g, 2, 9, count=40)
+    bc = H.elastic_bc(g, "x_lo", pins=[(g.node(202, 0), 1, 0.0), (g.node(100, 40), 0, 0.01)])
+    e, v = P.make_constraints(g, bc, 2)
+    u0 = H.random_field(2 * g.num_nodes, 10, -1e-3, 1e-3)
+    u0[e] = v
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=n_apt, n_pt=n_pt, form=form)
+    a, _ = _elastic2d_ctx_solve(g, E, f, bc, u0, p, True)
+    b, _ = _elastic2d_ctx_solve(g, E, f, bc, u0, p, False)
+    assert rel_err(a.current, b.current) < 1e-13 and rel_err(a.previous, b.previous) < 1e-13
+    assert np.array_equal(a.current[e], v)
+    rc, wc, wp, _ = port.hybrid_solve(1, g, bc, E, 0.3, f, u0, u0, p)
+    assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
+
+
+def test_elastic2d_temporal_blocking_abort_state():
+    """An exploding 2D elasticity solve aborts at the same check_finite step with the
+    same buffers in the blocked and the per-step solve."""
+    g = P.Grid.make2d(120, 50, 2.0, 1.0)
+    E = H.random_modulus(g, 3)
+    bc = H.elastic_bc(g, "x_lo")
+    u0 = H.random_field(2 * g.num_nodes, 4, -1e-3, 1e-3)
+    e, v = P.make_constraints(g, bc, 2)
+    u0[e] = v
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=40.0 * h, theta=1.0, n_apt=2000, n_pt=0, form=0)
+    a, sa = _elastic2d_ctx_solve(g, E, np.zeros(2 * g.num_nodes), bc, u0, p, True)
+    b, sb = _elastic2d_ctx_solve(g, E, np.zeros(2 * g.num_nodes), bc, u0, p, False)
+    assert sa is not None and sa == sb and sa % 100 == 0
+    same = (a.current == b.current) | (np.isnan(a.current) & np.isnan(b.current))
+    assert same.all()
