@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
 constexpr int EK = 4;                              // steps per round (divides 100)
 constexpr int ERX = 64, ERY = 32, ERN = ERX * ERY;
 constexpr int ETX = ERX - 2 * EK, ETY = ERY - 2 * EK;  // owned tile 56 x 24
-constexpr int ETHREADS = 512, EROWS = ERY / (ETHREADS / ERX);  // 4 rows per thread
+constexpr int ETHREADS = 1024, EROWS = ERY / (ETHREADS / ERX);  // 4 rows per thread
 constexpr size_t E_SMEM = (size_t)ERN * (sizeof(double) * (3 * 2 + 1 + 2) + 1);
 
 __global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) {
@@ -487,24 +487,27 @@ __global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) 
                 double acc[EROWS][2];
 #pragma unroll
                 for (int h = 0; h < EROWS; ++h) acc[h][0] = acc[h][1] = 0.0;
-                double hi[3][2], lo[3][2];  // rows lcj + 1 and lcj at columns lx-1, lx, lx+1
-                {
-                    const int row = min(ly0 + EROWS, ERY - 1);
+                // per row and component: the differences and sums of horizontally
+                // adjacent nodes (u[x] - u[x+1], u[x] + u[x+1] for x = lx-1, lx), the
+                // operands of the modal coefficients, shared by the cells above and below
+                double hd[2][2], hs[2][2], ld[2][2], ls[2][2];
+                auto row_terms = [&](int row, double (&dd)[2][2], double (&sd)[2][2]) {
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        hi[d][0] = Ux[row * ERX + lx - 1 + d];
-                        hi[d][1] = Uy[row * ERX + lx - 1 + d];
+                    for (int c = 0; c < 2; ++c) {
+                        const double* u = (c ? Uy : Ux) + row * ERX + lx - 1;
+                        const double w0 = u[0], w1 = u[1], w2 = u[2];
+                        dd[0][c] = w0 - w1;
+                        sd[0][c] = w0 + w1;
+                        dd[1][c] = w1 - w2;
+                        sd[1][c] = w1 + w2;
                     }
-                }
+                };
+                row_terms(min(ly0 + EROWS, ERY - 1), hd, hs);
 #pragma unroll
                 for (int cr = EROWS; cr >= 0; --cr) {
                     const int lcj = ly0 - 1 + cr;
                     const int row = max(lcj, 0);
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        lo[d][0] = Ux[row * ERX + lx - 1 + d];
-                        lo[d][1] = Uy[row * ERX + lx - 1 + d];
-                    }
+                    row_terms(row, ld, ls);
                     const int gcj = ry0 + lcj;
                     const bool row_ok = lcj >= sub - 1 && lcj + 1 <= ERY - sub && gcj >= 0 && gcj <= g.ny - 2;
 #pragma unroll
@@ -513,11 +516,10 @@ __global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) 
                         if (!row_ok || gci < 0 || gci > g.nx - 2) continue;
                         double C[4][2];
 #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            const double v0 = lo[cc][c], v1 = lo[cc + 1][c], v2 = hi[cc][c], v3 = hi[cc + 1][c];
-                            C[1][c] = (v0 - v1) + (v2 - v3);
-                            C[2][c] = (v0 + v1) - (v2 + v3);
-                            C[3][c] = (v0 - v1) - (v2 - v3);
+                        for (int c = 0; c < 2; ++c) {  // corners v0 v1 (row lcj), v2 v3 (row lcj + 1)
+                            C[1][c] = ld[cc][c] + hd[cc][c];  // (v0 - v1) + (v2 - v3)
+                            C[2][c] = ls[cc][c] - hs[cc][c];  // (v0 + v1) - (v2 + v3)
+                            C[3][c] = ld[cc][c] - hd[cc][c];  // (v0 - v1) - (v2 - v3)
                         }
                         const double ec = EC[row * ERX + lx - 1 + cc];
                         const double F10 = ec * (kh[0] * C[1][0] + kh[1] * C[2][1]);
@@ -537,7 +539,9 @@ __global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) 
                         }
                     }
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) hi[d][0] = lo[d][0], hi[d][1] = lo[d][1];
+                    for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) hd[k2][c] = ld[k2][c], hs[k2][c] = ls[k2][c];
                 }
 #pragma unroll
                 for (int h = 0; h < EROWS; ++h) {
