@@ -400,3 +400,23 @@ def test_elastic2d_temporal_blocking_abort_state():
     assert sa is not None and sa == sb and sa % 100 == 0
     same = (a.current == b.current) | (np.isnan(a.current) & np.isnan(b.current))
     assert same.all()
+
+
+@pytest.mark.parametrize("nx,ny", [(56, 24), (57, 25), (112, 48), (3, 150), (300, 3), (5, 3)])
+def test_elastic2d_temporal_blocking_tile_edges(port, nx, ny):
+    """Grids at, just past and far below the 56 x 24 tile (single rows / columns of
+    tiles, three-node-wide grids): blocked = per-step = oracle."""
+    g = P.Grid.make2d(nx, ny, 1.0 + nx / 100.0, 1.0)
+    E = H.random_modulus(g, nx + ny)
+    f = H.sparse_loads(g, 2, 3, count=3)
+    bc = H.elastic_bc(g, "x_lo" if nx > 3 else "y_lo")
+    e, v = P.make_constraints(g, bc, 2)
+    u0 = H.random_field(2 * g.num_nodes, 12, -1e-3, 1e-3)
+    u0[e] = v
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=37, n_pt=9, form=1)
+    a, _ = _elastic2d_ctx_solve(g, E, f, bc, u0, p, True)
+    b, _ = _elastic2d_ctx_solve(g, E, f, bc, u0, p, False)
+    assert rel_err(a.current, b.current) < 1e-13 and rel_err(a.previous, b.previous) < 1e-13
+    rc, wc, wp, _ = port.hybrid_solve(1, g, bc, E, 0.3, f, u0, u0, p)
+    assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
