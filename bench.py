@@ -372,7 +372,9 @@ def run_ours(a):
     if os.path.exists(prof):
         with open(prof) as f:
             d = json.load(f)
-        traffic = d.get(kname, {}).get("dram_bytes_per_launch")
+        cap = d.get(kname, {})
+        if cap.get("config", "C5") == a.config and world == 1:  # the capture's own workload only
+            traffic = cap.get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
