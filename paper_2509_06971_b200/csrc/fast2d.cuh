@@ -409,15 +409,21 @@ __global__ void __launch_bounds__(TB_THREADS, 1) k_heat2d_tb(const TBParams S) {
 // EK-node halo -- with elastic2d_node's arithmetic per node (the four cells
 // around it in the modal basis, state_solver.hpp:327-385 via stiffness.hpp).
 // Shared memory holds the three displacement levels, the cell moduli (corner sum
-// x scale, once per solve), the pinned values / loads and the mask; 512 threads,
-// each a column of four consecutive region rows.
+// x scale, once per solve), the pinned values / loads and the mask.
 constexpr int EK = 4;                              // steps per round (divides 100)
-constexpr int ERX = 64, ERY = 32, ERN = ERX * ERY;
-constexpr int ETX = ERX - 2 * EK, ETY = ERY - 2 * EK;  // owned tile 56 x 24
-constexpr int ETHREADS = 1024, EROWS = ERY / (ETHREADS / ERX);  // 4 rows per thread
-constexpr size_t E_SMEM = (size_t)ERN * (sizeof(double) * (3 * 2 + 1 + 2) + 1);
+// Region 64 x 16 ER: a thread per column and ER consecutive rows.  ER = 2 (tile
+// 56 x 24) for grids up to ~148 such tiles; ER = 1 (tile 56 x 8) halves each
+// thread's per-step chain for grids that fit in 148 of the smaller tiles (C1).
+constexpr int ERX = 64, ETX = ERX - 2 * EK, ETHREADS = 1024;
+__host__ __device__ constexpr int e_ry(int er) { return 16 * er; }
+__host__ __device__ constexpr int e_ty(int er) { return e_ry(er) - 2 * EK; }
+__host__ __device__ constexpr size_t e_smem(int er) {
+    return (size_t)ERX * e_ry(er) * (sizeof(double) * (3 * 2 + 1 + 2) + 1);
+}
 
+template <int ER>
 __global__ void __launch_bounds__(ETHREADS, 1) k_elastic2d_tb(const TBParams S) {
+    constexpr int ERY = e_ry(ER), ERN = ERX * ERY, ETY = e_ty(ER), EROWS = ER;
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     extern __shared__ __align__(16) unsigned char tb_smem[];
     double* U = reinterpret_cast<double*>(tb_smem);  // [3 levels][2 comps][ERN]

@@ -1237,16 +1237,28 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
     const bool heat = ctx->desc.physics == 0;
     if (ctx->g.dim == 2 && !ctx->no_tblock) {
         // temporal blocking: TBK (heat) / EK (elasticity) steps per grid barrier on
-        // shared-memory tiles
+        // shared-memory tiles; the first shape whose tiles are all co-resident
         const Geo& g = ctx->g;
-        const void* tfn = heat ? (const void*)k_heat2d_tb : (const void*)k_elastic2d_tb;
-        const int tiw = heat ? TBX : ETX, tih = heat ? TBY : ETY, nthr = heat ? TB_THREADS : ETHREADS;
-        const int tx = (g.nx + tiw - 1) / tiw, ty = (g.ny + tih - 1) / tih;
-        const size_t smem = heat ? (size_t)TRN * (6 * sizeof(double) + 1) : E_SMEM;
-        CK(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tfn, nthr, smem));
-        if ((long long)tx * ty <= (long long)per_sm * ctx->nsm) {
+        struct Shape {
+            const void* fn;
+            int tw, th, nthr;
+            size_t smem;
+            const char* name;
+        };
+        const Shape shapes[] = {
+            heat ? Shape{(const void*)k_heat2d_tb, TBX, TBY, TB_THREADS, (size_t)TRN * (6 * sizeof(double) + 1),
+                         "k_heat2d_tb"}
+                 : Shape{(const void*)k_elastic2d_tb<1>, ETX, e_ty(1), ETHREADS, e_smem(1), "k_elastic2d_tb"},
+            heat ? Shape{nullptr, 0, 0, 0, 0, nullptr}
+                 : Shape{(const void*)k_elastic2d_tb<2>, ETX, e_ty(2), ETHREADS, e_smem(2), "k_elastic2d_tb"},
+        };
+        for (const Shape& sh : shapes) {
+            if (!sh.fn) continue;
+            const int tx = (g.nx + sh.tw - 1) / sh.tw, ty = (g.ny + sh.th - 1) / sh.th;
+            CK(cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.nthr, sh.smem));
+            if ((long long)tx * ty > (long long)per_sm * ctx->nsm) continue;
             TBParams T{};
             T.base = S.base;
             T.pair[0][0] = S.st[0];
@@ -1264,9 +1276,8 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
             void* targs[] = {&T};
             cudaEvent_t ev[2];
             timing_begin(ctx, ev);
-            CK(cudaLaunchCooperativeKernel(tfn, dim3(tx * ty), dim3(nthr), targs, smem, ctx->stream));
-            timing_end(ctx, ev, heat ? "k_heat2d_tb" : "k_elastic2d_tb",
-                       (double)owned_nodes(ctx) * (heat ? 33.0 : 57.0) * (double)(n_apt + n_pt));
+            CK(cudaLaunchCooperativeKernel(sh.fn, dim3(tx * ty), dim3(sh.nthr), targs, sh.smem, ctx->stream));
+            timing_end(ctx, ev, sh.name, (double)owned_nodes(ctx) * (heat ? 33.0 : 57.0) * (double)(n_apt + n_pt));
             ctx->launches++;
             CKL();
             return PETTO_OK;

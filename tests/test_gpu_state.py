@@ -363,7 +363,7 @@ def _elastic2d_ctx_solve(g, E, f, bc, u0, p, tblock):
 
 @pytest.mark.parametrize("form,n_apt,n_pt", [(1, 137, 63), (0, 95, 0), (0, 0, 110), (1, 3, 2)])
 def test_elastic2d_temporal_blocking_matches_per_step_solve(port, form, n_apt, n_pt):
-    """The temporally blocked 2D elasticity solve (4 steps per grid barrier, 56 x 24
+    """The temporally blocked 2D elasticity solve (4 steps per grid barrier, 56 x 8
     tiles with a 4-node halo) against the per-step solve and the oracle: many tiles,
     ragged edges, a random modulus, point loads, a clamped face plus single-component
     pins, both APT forms, pure PT, rounds straddling the APT -> PT switch."""
@@ -402,10 +402,11 @@ def test_elastic2d_temporal_blocking_abort_state():
     assert same.all()
 
 
-@pytest.mark.parametrize("nx,ny", [(56, 24), (57, 25), (112, 48), (3, 150), (300, 3), (5, 3)])
+@pytest.mark.parametrize("nx,ny", [(56, 24), (57, 25), (112, 48), (3, 150), (300, 3), (5, 3), (400, 200), (113, 430)])
 def test_elastic2d_temporal_blocking_tile_edges(port, nx, ny):
-    """Grids at, just past and far below the 56 x 24 tile (single rows / columns of
-    tiles, three-node-wide grids): blocked = per-step = oracle."""
+    """Grids at, just past and far below the tile sizes (56 x 8 for grids that fit
+    148 of them, else 56 x 24: the last two grids), single rows / columns of tiles,
+    three-node-wide grids: blocked = per-step = oracle."""
     g = P.Grid.make2d(nx, ny, 1.0 + nx / 100.0, 1.0)
     E = H.random_modulus(g, nx + ny)
     f = H.sparse_loads(g, 2, 3, count=3)
