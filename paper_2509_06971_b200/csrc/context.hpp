@@ -123,6 +123,7 @@ struct petto_ctx {
     // instrumentation
     unsigned long long* cta_probe = nullptr;  // probe builds only (E3_CTA_TIMING)
     bool no_tblock = false;                   // PETTO_NO_TBLOCK=1: per-step grid barriers for 2D heat
+    bool no_pdl = false;                      // PETTO_NO_PDL=1: plain stream order between fused 3D steps
     long long launches = 0;
     bool timing = false;
     int timing_stride = 1;      // events around every timing_stride-th timed launch

@@ -479,6 +479,20 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
             cfg.dynamicSmemBytes = e3::SMEM_BYTES;
             cfg.stream = ctx->stream;
             timing_begin(ctx, ev);
+            // Programmatic dependent launch: step s+1's CTAs become resident on the SMs
+            // step s leaves idle and finish their setup (TMEM, barriers, tensor maps)
+            // before griddepcontrol.wait releases them at step s's completion.  Only
+            // when the plan leaves SMs idle (C4: 110 of 148; at C5 every SM is busy
+            // and it measured 0.7% slower), not on a launch whose duration is sampled,
+            // and not on slab ranks, whose steps are separated by stream memory
+            // operations.
+            cudaLaunchAttribute la[1];
+            if (!ctx->no_pdl && !ctx->peer_step && grid < ctx->nsm && !ev[0]) {
+                la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                la[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = la;
+                cfg.numAttrs = 1;
+            }
             cudaError_t le;
             // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
             switch (k.form * 2 + (partials ? 1 : 0)) {
@@ -867,6 +881,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     cudaMemsetAsync(ctx->r, 0, fb * ctx->comps, ctx->stream);
     ctx->npartials = std::max(4 * ctx->nsm, 1024);
     if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D solves
+    if (const char* e = std::getenv("PETTO_NO_PDL")) ctx->no_pdl = e[0] == '1';        // A/B of the 3D step overlap
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
         cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
