@@ -425,9 +425,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
-    // the next step may launch now (its CTAs wait in griddepcontrol.wait below until
-    // this grid has completed and its stores are visible)
+    // Programmatic dependent launch: the next step may launch now; this one waits
+    // until the previous step has completed and its stores are visible (a no-op
+    // without the launch attribute).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (skip_step(P.status, P.step, P.nsteps)) return;
 #ifdef E3_CTA_TIMING
     unsigned long long t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -446,11 +449,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         prefetch_tmap(&M.o);
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-    }
-    // everything below reads the previous step's output (or overwrites what it read)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const bool skip = skip_step(P.status, P.step, P.nsteps);
-    if (w == 8 && l == 0 && !skip) {
         pc->item = blockIdx.x;
         pc->t = 0;
         pc->kk = 0;
@@ -464,10 +462,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     __syncthreads();
     tmem_fence_after();
     const uint32_t tbase = *tslot;
-    if (skip) {  // uniform over the CTA: release tensor memory and leave
-        if (w == 0) tmem_dealloc(tbase, TMEM_COLS);
-        return;
-    }
     double rsq = 0.0;
     unsigned bad = 0;
 
