@@ -33,7 +33,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "APT stencil updates/s (GLUPS) and % HBM roofline at 1/2/4/8 B200 vs host-CPU"
 UNIT = "GLUPS"
-APT_BYTES_PER_NODE = 80.0  # u_n 24 + u_{n-1} 24 + E 8 + u_{n+1} 24
 
 
 def args_():
@@ -77,14 +76,17 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def workload(name):
-    """Assemble the configured problem exactly as the reference's build_problem would."""
-    from paper_2509_06971_b200 import device as D
+def workload(name, spectral_bound):
+    """Assemble the configured problem exactly as the reference's build_problem would.
+
+    spectral_bound is elasticity_spectral_bound (state_solver.hpp:254-279): the
+    product's (paper_2509_06971_b200.device) for our arm, the reference build's
+    (oracle/_ref) for the reference arm, so that arm never loads our library."""
     from paper_2509_06971_b200 import problem as P
 
     cfg = P.config(name)
     prob = P.build_problem(cfg)
-    sched = P.build_schedule(cfg, prob.grid, spectral_bound=D.spectral_bound)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=spectral_bound)
     g = prob.grid
     N = g.num_nodes
     # interpolate_into (objectives.hpp:95-116) of the initial design
@@ -93,6 +95,25 @@ def workload(name):
         E += p * prob.initial_phases[i * N:(i + 1) * N] ** 3
     E = np.maximum(E, prob.void_floor)
     return cfg, prob, sched, E
+
+
+def step_bytes(prob, form):
+    """Algorithmic HBM bytes per node and APT step: u_n, u_{n-1}, the
+    property and u_{n+1} -- 80 B for 3D elasticity, 56 B 2D elasticity, 32 B heat."""
+    lvl = 8 * prob.comps
+    return 3 * lvl + 8 if form in (0, 1) else 2 * lvl + 8
+
+
+def config_dict(a, cfg, prob, sched, world):
+    """The workload description both arms print (identical dicts: same_config)."""
+    g = prob.grid
+    dims = "x".join(str(n) for n in g.n[:g.dim])
+    return {"workload": f"{a.config}: {dims} {cfg.preset} {'heat' if prob.physics == 0 else 'elasticity'} "
+                        f"({g.num_nodes} nodes), hybrid_solve with n_apt={a.n_apt}, n_pt=0, "
+                        f"form={'semi_implicit' if sched.pt.form else 'explicit'}",
+            "l2": ("inputs larger than L2 (state 2x805 MB + modulus 268 MB per step)" if g.num_nodes > 8 << 20
+                   else "working set L2-resident (grid smaller than L2); no flush"),
+            "parallelism": "1 GPU" if world == 1 else f"slab{world}: grid split along its outermost axis"}
 
 
 class ClockSampler:
@@ -162,51 +183,70 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(name, prob, sched, E, steps, kind_pref="reference"):
-    """The reference's own OpenMP CPU path (oracle/_ref) on a bounded sample."""
+def cpu_baseline(name, prob, sched, E, steps=None, budget_s=1.0):
+    """The reference's own OpenMP CPU path (oracle/_ref, all host cores) on a bounded
+    sample: `steps` APT steps of the full grid, or as many as fit in ~budget_s."""
     from oracle import oracle as O
     from paper_2509_06971_b200 import problem as P
 
-    if kind_pref == "reference" and O.has_reference():
+    if O.has_reference():
         orc, kind, cores = O.load("reference"), "reference", host_threads()
         orc.set_threads(cores)
     else:
         orc, kind, cores = O.load("port"), "port", 1
     g = prob.grid
-    p = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, steps, 0, sched.pt.form)
-    sec = orc.time_hybrid(prob.physics, g, prob.bc, E, prob.poisson_ratio, prob.source, prob.initial_state,
-                          prob.initial_state, p)
+
+    def timed(n):
+        p = P.PTParams(sched.pt.dt_pt, sched.pt.dt_apt, sched.pt.theta, n, 0, sched.pt.form)
+        return orc.time_hybrid(prob.physics, g, prob.bc, E, prob.poisson_ratio, prob.source, prob.initial_state,
+                               prob.initial_state, p)
+
+    if steps is None:
+        t1 = timed(1)
+        steps = int(max(1, min(2000, budget_s / max(t1, 1e-9))))
+    sec = timed(steps)
     value = g.num_nodes * steps / sec / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{steps} APT steps of {name} ({g.n[0]}x{g.n[1]}x{g.n[2]}), {sec:.2f} s"}
+            "sample": f"{steps} APT steps of the full {name} grid ({'x'.join(str(n) for n in g.n[:g.dim])}), "
+                      f"{sec:.2f} s"}
 
 
 def run_reference(a):
+    """The reference arm: the reference's CPU implementation (oracle/_ref) on the same
+    config; nothing of this repo's library is loaded (the schedule's spectral bound
+    comes from the reference build too)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    cfg, prob, sched, E = workload(a.config)
-    g = prob.grid
-    vals = []
     from oracle import oracle as O
 
     if not O.has_reference():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
         return 0
+    ref = O.load("reference")
+    ref.set_threads(host_threads())
+    cfg, prob, sched, E = workload(a.config, ref.spectral_bound)
+    g = prob.grid
+    # one bench step = a bounded sample of the workload: as many APT steps of the
+    # full grid as take ~2 s on the host cores (C5: one step is ~2-4 s)
+    steps = None
+    vals, samples = [], []
     for it in range(a.warmup + a.steps):
-        cb = cpu_baseline(a.config, prob, sched, E, 1)
+        cb = cpu_baseline(a.config, prob, sched, E, steps, budget_s=2.0)
+        if steps is None:
+            steps = int(cb["sample"].split()[0])
         if it >= a.warmup:
             vals.append(cb["value"])
+            samples.append(cb["sample"])
     v = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": g.num_nodes / (v * 1e9) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (reference {a.config} problem)",
-        "config": {"workload": f"{a.config}: {cfg.nx}x{cfg.ny}x{cfg.nz} {cfg.preset} "
-                               f"{'heat' if prob.physics == 0 else 'elasticity'}, APT steps",
-                   "sample": "1 APT step per bench step"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
-                         "sample": "1 APT step of the full grid per bench step"},
+        "warmup": a.warmup, "ms_per_step": g.num_nodes * a.n_apt / (v * 1e9) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (reference {a.config} problem: initial design, zero state)",
+        "config": config_dict(a, cfg, prob, sched, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "reference",
+                         "sample": f"per bench step: {samples[-1]} (oracle/_ref, OpenMP)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -227,7 +267,7 @@ def run_ours(a):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg, prob, sched, E = workload(a.config)
+    cfg, prob, sched, E = workload(a.config, D.spectral_bound)
     g = prob.grid
     N = g.num_nodes
     comps = prob.comps
@@ -300,8 +340,17 @@ def run_ours(a):
     total_updates = N * a.n_apt * a.steps  # strong scaling: the whole grid, all ranks together
     value = total_updates / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
-    avg_launch_s = kms * 1e-3 / max(klaunch, 1) if klaunch else ms * 1e-3 / max(launches, 1)
-    achieved = N_local * APT_BYTES_PER_NODE / avg_launch_s / 1e9  # this rank's kernel
+    # achieved = algorithmic bytes of one launch (per-physics bytes/node x nodes x the
+    # steps that launch runs: 1 for the fused 3D kernel, the whole solve for the
+    # cooperative 2D/heat kernels) / its mean duration, from CUDA events on the
+    # context's stream inside the timed region
+    if klaunch:
+        avg_launch_s = kms * 1e-3 / klaunch
+        launch_bytes = kbytes
+    else:  # no sampled launch: the step time over the step's bytes
+        avg_launch_s = ms * 1e-3 / a.steps
+        launch_bytes = N_local * step_bytes(prob, sched.pt.form) * a.n_apt
+    achieved = launch_bytes / avg_launch_s / 1e9  # this rank's kernel
 
     # e2e: the same hybrid_solve through the C-ABI with host buffers.  Every step
     # uploads u_n, u_{n-1} from pinned memory, solves and downloads both.  On one
@@ -366,6 +415,16 @@ def run_ours(a):
                "h2d_bytes_per_step": 2 * moved, "d2h_bytes_per_step": 2 * comps * N * 8,
                "steps": e2e_steps, "pipeline": f"{pipe} contexts from {pipe} host threads"
                if pipe > 1 else "sequential"}
+        if pipe > 1:
+            # what one drop-in caller sees: one context, upload -> solve -> download in turn
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            n1 = max(2, e2e_steps // pipe)
+            for _ in range(n1):
+                e2e_step(0)
+            torch.cuda.synchronize()
+            e2e["single_context"] = {"value": N * a.n_apt * n1 / (time.perf_counter() - t0) / 1e9, "unit": UNIT,
+                                     "steps": n1, "pipeline": "sequential (one context, one host thread)"}
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -380,25 +439,20 @@ def run_ours(a):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (reference {a.config} problem: initial design, zero state)",
-        "config": {"workload": f"{a.config}: {g.n[0]}x{g.n[1]}x{g.n[2]} {cfg.preset} "
-                               f"{'heat' if prob.physics == 0 else 'elasticity'} "
-                               f"({N} nodes), hybrid_solve with n_apt={a.n_apt}, n_pt=0, "
-                               f"form={'semi_implicit' if sched.pt.form else 'explicit'}",
-                   "l2": "inputs larger than L2 (state 2x805 MB + modulus 268 MB per step)",
-                   "parallelism": "1 GPU" if world == 1 else
-                   f"slab{world}: z planes split over {world} GPUs, ghost planes by "
-                   + ("peer stores from the fused kernel (CUDA IPC, NVLink)" if a.halo == "peer" else
-                      "NCCL send/recv every step")},
+        "config": config_dict(a, cfg, prob, sched, world),
+        "halo": None if world == 1 else ("peer stores from the fused kernel (CUDA IPC, NVLink)" if a.halo == "peer"
+                                         else "NCCL send/recv every step"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kname, "peak_source": peak_kind,
-                     "bytes_per_node": APT_BYTES_PER_NODE, "avg_launch_ms": avg_launch_s * 1e3},
+                     "bytes_per_node_step": step_bytes(prob, sched.pt.form), "bytes_per_launch": launch_bytes,
+                     "avg_launch_ms": avg_launch_s * 1e3},
         "gpu_launches": int(launches),
         "e2e": e2e,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not a.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_baseline(a.config, prob, sched, E, a.cpu_steps)
+            line["cpu_baseline"] = cpu_baseline(a.config, prob, sched, E, a.cpu_steps if a.config == "C5" else None)
         except Exception as ex:  # noqa: BLE001
             line["cpu_baseline"] = {"error": str(ex)}
     if rank == 0:

@@ -333,6 +333,17 @@ void plan_3d(const petto_ctx* ctx, int nstrips, int& chunk, int& nitems, int& gr
     grid = std::min(ctx->nsm, nitems);
 }
 
+// Algorithmic HBM bytes per node and pseudo-time step: every
+// array touched once -- state levels, the property, the new level.  Loads, pins
+// and 1/V are O(surface) or computed and not counted.
+double step_bytes(const petto_ctx* ctx, int form) {
+    const int c = ctx->comps;
+    const double lvl = 8.0 * c;                   // one state level
+    if (form == 3) return lvl + 8.0 + lvl;        // residual: u_n, property, r
+    if (form == 2) return lvl + 8.0 + lvl;        // PT: u_n, property, u_{n+1}
+    return lvl + lvl + 8.0 + lvl;                 // APT: u_n, u_{n-1}, property, u_{n+1}
+}
+
 void timing_begin(petto_ctx* ctx, cudaEvent_t* ev) {
     ev[0] = ev[1] = nullptr;
     if (!ctx->timing) return;
@@ -506,7 +517,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
                 default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true>, P, M); break;
             }
             if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
-            timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * (k.form <= 1 ? 81.0 : 57.0));
+            timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * step_bytes(ctx, k.form));
             ctx->launches++;
             CKL();
             if (partials) ctx->npartials_used = grid;
@@ -517,10 +528,10 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
         timing_begin(ctx, ev);
         if (ctx->desc.physics == 0) {
             k_heat_fast<<<grid, 256, 0, ctx->stream>>>(P);
-            timing_end(ctx, ev, "k_heat_fast", (double)owned * (k.form <= 1 ? 33.0 : 25.0));
+            timing_end(ctx, ev, "k_heat_fast", (double)owned * step_bytes(ctx, k.form));
         } else {
             k_elastic2d_fast<<<grid, 256, 0, ctx->stream>>>(P);
-            timing_end(ctx, ev, "k_elastic2d_fast", (double)owned * (k.form <= 1 ? 57.0 : 41.0));
+            timing_end(ctx, ev, "k_elastic2d_fast", (double)owned * step_bytes(ctx, k.form));
         }
         ctx->launches++;
         CKL();
@@ -1292,7 +1303,8 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
             cudaEvent_t ev[2];
             timing_begin(ctx, ev);
             CK(cudaLaunchCooperativeKernel(sh.fn, dim3(tx * ty), dim3(sh.nthr), targs, sh.smem, ctx->stream));
-            timing_end(ctx, ev, sh.name, (double)owned_nodes(ctx) * (heat ? 33.0 : 57.0) * (double)(n_apt + n_pt));
+            timing_end(ctx, ev, sh.name,
+                       (double)owned_nodes(ctx) * (step_bytes(ctx, ka.form) * n_apt + step_bytes(ctx, 2) * n_pt));
             ctx->launches++;
             CKL();
             return PETTO_OK;
@@ -1306,8 +1318,8 @@ int small_solve(petto_ctx* ctx, const StepCoef& ka, const StepCoef& kp, long lon
     cudaEvent_t ev[2];
     timing_begin(ctx, ev);
     CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, ctx->stream));
-    const double bpn = heat ? 33.0 : 57.0;  // APT bytes per node
-    timing_end(ctx, ev, "k_small_solve", (double)owned_nodes(ctx) * bpn * (double)(n_apt + n_pt));
+    timing_end(ctx, ev, "k_small_solve",
+               (double)owned_nodes(ctx) * (step_bytes(ctx, ka.form) * n_apt + step_bytes(ctx, 2) * n_pt));
     ctx->launches++;
     CKL();
     return PETTO_OK;

@@ -1,0 +1,160 @@
+"""The north-star parity gate (BASELINE.json north_star) on the
+BASELINE configs at their stated sizes: the device run() against the reference's
+own run() (optimizer.hpp:120-223), fixtures from tests/golden/make_golden_n1.py.
+
+Gate: per-outer-iteration compliance and volume fractions within
+1e-8 relative, the final density field within 1e-7 max-abs (two reference runs
+differ by ~2e-8 on C4), the APT iteration count to tolerance +-1.
+Windows: heat C2 40 loops, 2D cantilever / MBB C1, C3 100 loops,
+3D cantilever C4 all 200 loops, C5 one full loop (100 APT + 100 PT).
+
+The CPU tests pin the fixtures (schedule, record layout) and replay the first
+loops of C1 through the C restatement; the GPU tests are the gate itself.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2509_06971_b200 import problem as P
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+N1 = os.path.join(HERE, "golden", "n1")
+CASES = ["C1", "C2", "C3", "C4", "C5"]
+Q = float(2 ** 32 - 1)
+
+REL_GATE = 1e-8   # per-loop compliance / volume fractions
+PHI_GATE = 1e-7   # final density, max-abs
+
+
+def fixture(name):
+    p = os.path.join(N1, f"{name}.json")
+    if not os.path.exists(p):
+        pytest.skip(f"fixture {name} not generated (tests/golden/make_golden_n1.py {name})")
+    with open(p) as f:
+        d = json.load(f)
+    d["phi"] = np.load(os.path.join(N1, f"{name}_phi.npz"))["q"].astype(np.float64) / Q
+    return d
+
+
+def problem_of(d, spectral_bound):
+    cfg = P.config(d["config"], **d["overrides"])
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=spectral_bound)
+    return prob, sched
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def record_drift(recs, want):
+    """max relative difference per observable over the records."""
+    out = {"compliance": 0.0, "volume_fractions": 0.0}
+    for a, b in zip(recs, want):
+        assert a.loop == b["loop"]
+        out["compliance"] = max(out["compliance"], rel(a.compliance, b["compliance"]))
+        for q, v in enumerate(b["volume_fractions"]):
+            out["volume_fractions"] = max(out["volume_fractions"], rel(a.volume_fractions[q], v))
+    return out
+
+
+# ------------------------------------------------------------------ CPU side
+
+@pytest.mark.parametrize("name", CASES)
+def test_fixture_schedule_matches_problem_assembly(port, name):
+    """The fixture's schedule is the one problem.build_schedule derives (same
+    spectral bound through the C restatement), and it records every loop."""
+    d = fixture(name)
+    prob, sched = problem_of(d, port.spectral_bound)
+    s = d["schedule"]
+    assert (sched.pt.n_apt, sched.pt.n_pt, sched.pt.form) == (s["n_apt"], s["n_pt"], s["form"])
+    for k in ("dt_apt", "dt_pt", "theta"):
+        assert getattr(sched.pt, k) == s[k], k
+    assert sched.dt_ch == s["dt_ch"]
+    assert len(d["records"]) == d["loops"] == d["overrides"]["max_loops"]
+    assert d["phi"].shape[0] == prob.nphases
+    assert np.all((d["phi"] >= 0) & (d["phi"] <= 1))
+
+
+def test_port_replays_c1_fixture(port):
+    """The C restatement reproduces the reference's C1 trajectory (first 12 loops)."""
+    d = fixture("C1")
+    cfg = P.config("C1", max_loops=12, report_every=1)
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=port.spectral_bound)
+    _, _, recs, res = port.run(prob, sched)
+    assert res.loops == 12
+    for a, b in zip(recs, d["records"][:12]):
+        assert a.loop == b["loop"]
+        assert a.compliance == b["compliance"]
+        assert list(a.volume_fractions)[:prob.nphases] == b["volume_fractions"]
+
+
+# ------------------------------------------------------------------ GPU gate
+
+def _device():
+    from paper_2509_06971_b200 import device as D
+
+    return D
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fast", "replica"])
+@pytest.mark.parametrize("name", CASES)
+def test_run_matches_reference_at_stated_size(name, mode):
+    D = _device()
+    d = fixture(name)
+    prob, sched = problem_of(d, D.spectral_bound)
+    ctx = D.Context.from_problem(prob, D.MODE_FAST if mode == "fast" else D.MODE_REPLICA)
+    res, recs = ctx.run(sched)
+    assert (res.loops, res.termination, res.apt_steps, res.pt_steps) == (
+        d["loops"], d["termination"], d["apt_steps"], d["pt_steps"])
+    assert len(recs) == len(d["records"])
+    drift = record_drift(recs, d["records"])
+    N = prob.grid.num_nodes
+    phi = ctx.get_phases().reshape(prob.nphases, N)
+    if "phi_stride" in d:
+        phi = phi[:, ::d["phi_stride"]]
+    dphi = float(np.abs(phi - d["phi"]).max())
+    print(f"N1 {name} {mode}: loops {res.loops} max rel compliance {drift['compliance']:.3e} "
+          f"volfrac {drift['volume_fractions']:.3e} final phi max-abs {dphi:.3e}")
+    assert drift["compliance"] <= REL_GATE, drift
+    assert drift["volume_fractions"] <= REL_GATE, drift
+    assert dphi <= PHI_GATE
+    assert abs(res.clamp_mass_drift - d["clamp_mass_drift"]) <= 1e-8 * max(abs(d["clamp_mass_drift"]), 1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fast", "replica"])
+def test_elastic_iteration_count_at_c4(mode):
+    """iterate_to_tolerance (state_solver.hpp:511-541), APT, on the C4 problem: the
+    same iteration count as the reference +-1."""
+    D = _device()
+    d = fixture_tol()
+    cfg = P.config("C4")
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=D.spectral_bound)
+    ctx = D.Context.from_problem(prob, D.MODE_FAST if mode == "fast" else D.MODE_REPLICA)
+    ctx.interpolate()
+    ctx.init_operator()
+    z = np.zeros(3 * prob.grid.num_nodes)
+    ctx.set_state(z, z)
+    st = ctx.iterate_to_tolerance(1, sched.pt, d["target"], 40000)
+    print(f"C4 tolerance {mode}: {st.iterations} iterations (reference {d['iterations']}), "
+          f"r_final {st.r_final:.6e} (reference {d['r_final']:.6e})")
+    assert bool(st.converged) == bool(d["converged"])
+    assert rel(st.r_initial, d["r_initial"]) < 1e-12
+    if mode == "replica":
+        assert st.iterations == d["iterations"]
+    else:
+        assert abs(st.iterations - d["iterations"]) <= 1
+
+
+def fixture_tol():
+    p = os.path.join(N1, "C4tol.json")
+    if not os.path.exists(p):
+        pytest.skip("fixture C4tol not generated")
+    with open(p) as f:
+        return json.load(f)
