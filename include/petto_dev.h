@@ -222,8 +222,11 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
  *
  * Multi-process (one GPU per rank): rank 0 creates a 128-byte NCCL unique id, the
  * caller broadcasts it, every rank calls petto_dev_comm_init.  From then on the
- * state solves exchange ghost planes with the +-1 ranks after every step and
- * all-reduce the residual norms, masses, maxima and objective sums. */
+ * state solves exchange ghost planes with the +-1 ranks after every step, the
+ * design loop exchanges the ghost planes of phi and mu around the Cahn-Hilliard
+ * kernels, and every global scalar (r^2, the first non-finite step at each
+ * check_finite, masses, max|gc|, compliance/unity/region sums, the separation
+ * count) is all-reduced -- REPLICA sums as one serial sum passed rank to rank. */
 int petto_dev_comm_unique_id(void* id128);
 int petto_dev_comm_init(petto_ctx* ctx, const void* id128, int rank, int nranks);
 
@@ -239,11 +242,25 @@ int petto_dev_peer_export(petto_ctx* ctx, void* blob);
 int petto_dev_peer_import(petto_ctx* ctx, const void* lo_blob, const void* hi_blob);
 
 /* Single process driving several contexts (several GPUs, or one GPU in tests):
- * link the contexts of consecutive slabs, then solve them in lock step: fused 3D
- * steps use the peer halo (direct pointers), the other kernels stream-ordered
- * peer copies of the ghost planes. */
+ * link the contexts of consecutive slabs, then run them in lock step -- the same
+ * solver and design-loop code as one context or one NCCL rank, with the group's
+ * own transport: fused 3D steps use the peer halo (direct pointers), the other
+ * kernels stream-ordered peer copies of the ghost planes, and every reduction
+ * (r^2, first non-finite step, masses, max|gc|, compliance/unity/region sums,
+ * the separation count) is combined on the first context in slab order
+ * (REPLICA: one serial sum chained across the slabs, bit-identical to one
+ * domain).  A linked or communicator-less slab context is refused by the
+ * single-context entry points (PETTO_INVALID).  Results land in ctxs[0]. */
 int petto_dev_group_link(petto_ctx** ctxs, int n);
 int petto_dev_group_hybrid_solve(petto_ctx** ctxs, int n, const petto_pt_params* p, int64_t* abort_step);
+int petto_dev_group_residual(petto_ctx** ctxs, int n, double* r_pde);
+int petto_dev_group_interpolate(petto_ctx** ctxs, int n);
+int petto_dev_group_init_operator(petto_ctx** ctxs, int n); /* nu from node 0 on the first slab */
+int petto_dev_group_design_update(petto_ctx** ctxs, int n);
+int petto_dev_group_ch_step(petto_ctx** ctxs, int n, const petto_ch_params* p, petto_ch_stats* stats);
+int petto_dev_group_objectives(petto_ctx** ctxs, int n, petto_report* rep, double* separation);
+int petto_dev_group_run(petto_ctx** ctxs, int n, const petto_schedule* s, petto_record_cb cb, void* user,
+                        petto_run_result* result);
 
 /* --------------------------------------------------------------- utilities */
 

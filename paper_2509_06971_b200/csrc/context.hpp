@@ -109,6 +109,9 @@ struct petto_ctx {
     petto_ctx* nb_hi = nullptr;
     cudaEvent_t ev_step = nullptr;   // local group: this context's step finished
     cudaEvent_t ev_pull = nullptr;   // local group: this context's ghost pulls finished
+    cudaEvent_t ev_team = nullptr;   // local group: this context reached a team collective
+    void* team_buf = nullptr;        // local group lead: gathered values of a team reduction
+    bool phi_ghosts_stale = false;   // owned planes of the phases changed since the last phase halo
 
     // output writers (writers.cuh): two text buffers on each side for the
     // format -> copy -> write pipeline, per-block byte counts / offsets, scan scratch

@@ -140,10 +140,12 @@ __global__ void k_term_mass(Geo g, const double* __restrict__ phi, double* __res
     term[t] = rmul(phi[node], cell_volume(g, i, j, k));
 }
 
-// single-thread ordered sum (par::serial() branch) / fixed-shape tree partials
-__global__ void k_sum_serial(const double* __restrict__ term, long long n, double* out) {
+// single-thread ordered sum (par::serial() branch) / fixed-shape tree partials.
+// `init` continues a sum over the previous slabs (the team chain, REPLICA mode).
+__global__ void k_sum_serial(const double* __restrict__ term, long long n, double* out,
+                             const double* init = nullptr) {
     if (threadIdx.x || blockIdx.x) return;
-    double s = 0.0;
+    double s = init ? *init : 0.0;
     for (long long t = 0; t < n; ++t) s = radd(s, term[t]);
     *out = s;
 }
@@ -219,6 +221,8 @@ enum {
     DS_DRIFT = 64,   // accumulated clamp mass drift
     DS_CH = 72,      // [8][3] ch masses: before, pre, post
     DS_OBJ = 104,    // [4] compliance, unity, separation count, spare
+    DS_CHAIN = 108,  // running value of a team chain sum (REPLICA)
+    DS_CHAIN_IN = 109,
     DS_COUNT = 128
 };
 
@@ -231,12 +235,21 @@ struct UpdateScal {
     int normalize, sign;
 };
 
-__global__ void k_design_scalars(int np, UpdateScal u, double* dsc, const double* __restrict__ pmax, int nblocks) {
+// this slab's max|gc_i| (par::max_abs_nodes, parallel.hpp:33-42) from the block maxima
+__global__ void k_local_gmax(int np, const double* __restrict__ pmax, int nblocks, double* dsc) {
     if (threadIdx.x || blockIdx.x) return;
     for (int q = 0; q < np; ++q) {
         double m = 0.0;
         for (int b = 0; b < nblocks; ++b) m = fmax(m, pmax[b * 8 + q]);
         dsc[DS_GMAX + q] = m;
+    }
+}
+
+// dsc[DS_GMAX] holds the global maxima (team-reduced), dsc[DS_MASS] the masses
+__global__ void k_design_scalars(int np, UpdateScal u, double* dsc) {
+    if (threadIdx.x || blockIdx.x) return;
+    for (int q = 0; q < np; ++q) {
+        const double m = dsc[DS_GMAX + q];
         const double mean = dsc[DS_MASS + q] * u.inv_vol;  // volume_fractions
         dsc[DS_DM + q] = (2.0 * (mean - u.fractions[q])) * u.inv_vol;
         double cs = 0.0;
@@ -399,6 +412,35 @@ __global__ void k_objective_terms(Geo g, DesignP d, int kind, double cl, double 
     }
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, near));
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(sep_count, (unsigned long long)cnt);
+}
+
+// Team reduction on the group lead: n contexts' values gathered rank after rank,
+// combined in rank order (deterministic).  op: 0 sum f64, 1 max f64, 2 min i64,
+// 3 sum u64, 4 max u32.
+__global__ void k_team_combine(const void* __restrict__ buf, int n, int count, int op, void* out) {
+    const int v = threadIdx.x;
+    if (blockIdx.x || v >= count) return;
+    if (op == 0 || op == 1) {
+        const double* b = static_cast<const double*>(buf);
+        double a = b[v];
+        for (int r = 1; r < n; ++r) a = op == 0 ? radd(a, b[r * count + v]) : fmax(a, b[r * count + v]);
+        static_cast<double*>(out)[v] = a;
+    } else if (op == 2) {
+        const long long* b = static_cast<const long long*>(buf);
+        long long a = b[v];
+        for (int r = 1; r < n; ++r) a = min(a, b[r * count + v]);
+        static_cast<long long*>(out)[v] = a;
+    } else if (op == 3) {
+        const unsigned long long* b = static_cast<const unsigned long long*>(buf);
+        unsigned long long a = b[v];
+        for (int r = 1; r < n; ++r) a += b[r * count + v];
+        static_cast<unsigned long long*>(out)[v] = a;
+    } else {
+        const unsigned* b = static_cast<const unsigned*>(buf);
+        unsigned a = b[v];
+        for (int r = 1; r < n; ++r) a = max(a, b[r * count + v]);
+        static_cast<unsigned*>(out)[v] = a;
+    }
 }
 
 __global__ void k_check_finite_phases(Geo g, int np, const double* __restrict__ ph, unsigned* flag) {

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -629,15 +630,14 @@ int nccl_check(petto_ctx* ctx, ncclResult_t r, const char* what) {
 
 // Ghost planes of `field` from the +-1 ranks (NCCL transport), stream ordered after
 // the kernel that wrote the owned planes.  No-op on a single rank.
-int halo(petto_ctx* ctx, FieldSel s, int buf) {
+int halo_ptr(petto_ctx* ctx, double* f, int comps) {
     if (!ctx->nccl_comm) return PETTO_OK;
     NcclApi& N = nccl();
     const ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl_comm);
     const Geo& g = ctx->g;
-    double* f = field_of(ctx, s, buf);
     const size_t plane = (size_t)g.px * g.ny;
     N.GroupStart();
-    for (int c = 0; c < comps_of(ctx, s); ++c) {
+    for (int c = 0; c < comps; ++c) {
         double* fc = f + c * g.Ns;
         if (ctx->rank > 0) {
             N.Send(fc + lidx(g, 0, 0, g.kb), plane, ncclDouble, ctx->rank - 1, comm, ctx->stream);
@@ -650,6 +650,8 @@ int halo(petto_ctx* ctx, FieldSel s, int buf) {
     }
     return nccl_check(ctx, N.GroupEnd(), "halo exchange");
 }
+
+int halo(petto_ctx* ctx, FieldSel s, int buf) { return halo_ptr(ctx, field_of(ctx, s, buf), comps_of(ctx, s)); }
 
 // In-place all-reduce of device scalars across the ranks (no-op on one rank).
 int allreduce(petto_ctx* ctx, void* p, size_t n, ncclDataType_t t, ncclRedOp_t op) {
@@ -924,6 +926,8 @@ void petto_dev_destroy(petto_ctx* ctx) {
         if (nb) (nb->nb_lo == ctx ? nb->nb_lo : nb->nb_hi) = nullptr;
     if (ctx->ev_step) cudaEventDestroy(ctx->ev_step);
     if (ctx->ev_pull) cudaEventDestroy(ctx->ev_pull);
+    if (ctx->ev_team) cudaEventDestroy(ctx->ev_team);
+    cudaFree(ctx->team_buf);
     for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
     cudaFree(ctx->prop);
     cudaFree(ctx->ecell);
@@ -1182,28 +1186,6 @@ int petto_dev_get_state(petto_ctx* ctx, double* current, double* previous) {
     return PETTO_OK;
 }
 
-int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
-    CK(cudaSetDevice(ctx->device));
-    if (int rc = require_ready(ctx)) return rc;
-    if (int rc = check_kappa(ctx)) return rc;
-    if (int rc = reset_status(ctx)) return rc;
-    const StepCoef k = coef(3, 0.0, 1.0);
-    if (int rc = state_step(ctx, k, ctx->cur, ctx->prev, ctx->r, 0, 0, true)) return rc;
-    if (ctx->mode == PETTO_MODE_FAST) {
-        k_sum_to<<<1, 256, 0, ctx->stream>>>(ctx->partials, ctx->npartials_used, &ctx->status->sumsq);
-        ctx->launches++;
-        CKL();
-    }
-    if (int rc = allreduce(ctx, &ctx->status->sumsq, 1, ncclDouble, ncclSum)) return rc;
-    if (int rc = read_status(ctx)) return rc;
-    if (r_pde) *r_pde = std::sqrt(ctx->status_h->sumsq) / (double)global_nodes(ctx);
-    if (out) {
-        if (int rc = download(ctx, out, ctx->r, ctx->comps)) return rc;
-        CK(cudaStreamSynchronize(ctx->stream));
-    }
-    return PETTO_OK;
-}
-
 // Inbox of the peer halo: two step counters written by the neighbours.
 int peer_prepare(petto_ctx* ctx) {
     if (!ctx->inbox) {
@@ -1335,40 +1317,6 @@ static int validate_params(petto_ctx* ctx, const petto_pt_params* p) {
     return PETTO_OK;
 }
 
-int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* abort_step) {
-    CK(cudaSetDevice(ctx->device));
-    if (int rc = validate_params(ctx, p)) return rc;
-    if (int rc = require_ready(ctx)) return rc;
-    if (int rc = check_kappa(ctx)) return rc;
-    if (int rc = reset_status(ctx)) return rc;
-    const long long nsteps = p->n_apt + p->n_pt;
-    long long step = 0;
-    const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
-    const StepCoef kp = coef(2, p->dt_pt, p->theta);
-    if (small_solve_ok(ctx)) {
-        if (int rc = small_solve(ctx, ka, kp, p->n_apt, p->n_pt)) return rc;
-        if (nsteps % 2) std::swap(ctx->cur, ctx->prev);  // the kernel swapped nsteps times
-    }
-    for (long s = 0; s < p->n_apt && !small_solve_ok(ctx); ++s)
-        if (int rc = hybrid_step(ctx, ka, ++step, nsteps)) return rc;
-    for (long s = 0; s < p->n_pt && !small_solve_ok(ctx); ++s)
-        if (int rc = hybrid_step(ctx, kp, ++step, nsteps)) return rc;
-    // every rank aborts at the same check_finite step
-    if (int rc = allreduce(ctx, &ctx->status->first_bad, 1, ncclInt64, ncclMin)) return rc;
-    if (int rc = read_status(ctx)) return rc;
-    if (ctx->status_h->first_bad != PETTO_NO_BAD) {
-        const long long fb = ctx->status_h->first_bad;
-        long long at = std::min(((fb + 99) / 100) * 100, nsteps);
-        // the kernels after `at` were skipped: the buffers still hold the state of
-        // step `at`, but our cur/prev indices advanced past it -- rewind the swaps
-        if ((nsteps - at) % 2) std::swap(ctx->cur, ctx->prev);
-        if (abort_step) *abort_step = at;
-        return fail(ctx, PETTO_ABORT, "numerical abort in 'state' at step " + std::to_string(at) +
-                                          ": non-finite values (time step too large?)");
-    }
-    return PETTO_OK;
-}
-
 int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_params* p, double target,
                                    long max_iters, petto_solve_stats* stats) {
     CK(cudaSetDevice(ctx->device));
@@ -1465,47 +1413,6 @@ static double domain_volume(const petto_ctx* ctx) {
     return v;
 }
 
-// Ordered (REPLICA) or fixed-tree (FAST) sum of n terms into a device scalar.
-static int sum_terms(petto_ctx* ctx, const double* term, long long n, double* dst) {
-    if (ctx->mode == PETTO_MODE_REPLICA) {
-        k_sum_serial<<<1, 32, 0, ctx->stream>>>(term, n, dst);
-        ctx->launches++;
-    } else {
-        const int nb = (int)std::min<long long>(ctx->npartials, blocks_for(n));
-        k_sum_partials<<<nb, 256, 0, ctx->stream>>>(term, n, ctx->partials);
-        k_sum_finish<<<1, 256, 0, ctx->stream>>>(ctx->partials, nb, dst);
-        ctx->launches += 2;
-    }
-    CKL();
-    return PETTO_OK;
-}
-
-static int phase_masses(petto_ctx* ctx, int slot) {
-    const long long owned = owned_nodes(ctx);
-    for (int q = 0; q < ctx->mat.nphases; ++q) {
-        k_term_mass<<<blocks_for(owned), 256, 0, ctx->stream>>>(ctx->g, ctx->phases + q * ctx->g.Ns, ctx->term1);
-        ctx->launches++;
-        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + slot + q)) return rc;
-    }
-    return PETTO_OK;
-}
-
-static int region_sums(petto_ctx* ctx) {
-    if (!ctx->tgt.has_region) return PETTO_OK;
-    const long long n = (long long)ctx->region_nodes.size();
-    const int nb = blocks_for(n);
-    k_region_terms<<<nb, 256, 0, ctx->stream>>>(ctx->g, ctx->region_dev, n, nullptr, ctx->term1);
-    ctx->launches++;
-    if (int rc = sum_terms(ctx, ctx->term1, n, ctx->dscal + DS_RVOL)) return rc;
-    for (int q = 0; q < ctx->mat.nphases; ++q) {
-        k_region_terms<<<nb, 256, 0, ctx->stream>>>(ctx->g, ctx->region_dev, n, ctx->phases + q * ctx->g.Ns,
-                                                    ctx->term1);
-        ctx->launches++;
-        if (int rc = sum_terms(ctx, ctx->term1, n, ctx->dscal + DS_RACC + q)) return rc;
-    }
-    return PETTO_OK;
-}
-
 int petto_dev_set_design(petto_ctx* ctx, const petto_material* m, const petto_targets* t, const petto_weights* w) {
     CK(cudaSetDevice(ctx->device));
     if (int rc = validate_design(ctx, m, w)) return rc;
@@ -1577,38 +1484,464 @@ int petto_dev_get_phases(petto_ctx* ctx, double* phases) {
     return PETTO_OK;
 }
 
-int petto_dev_interpolate(petto_ctx* ctx, double* property_out) {
-    CK(cudaSetDevice(ctx->device));
-    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
-    const long long n = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nzs;
-    k_interpolate<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->g, design_params(ctx), ctx->phases, ctx->prop);
-    ctx->ecell_valid = false;
-    ctx->launches++;
-    CKL();
-    ctx->prop_node0_valid = false;
-    ctx->prop_is_mu = false;
-    if (property_out) {
-        if (int rc = download(ctx, property_out, ctx->prop, 1)) return rc;
-        CK(cudaStreamSynchronize(ctx->stream));
+// ================================================================= teams
+// A slab decomposition as one host thread drives it: the contexts that thread
+// owns -- every slab of a local group (one process, one or several GPUs), or this
+// rank's single context under NCCL -- and the transport between the slabs.  The
+// solver and design-loop routines below run the same code for one domain, a local
+// group and an NCCL rank.  Every collective is stream ordered, with
+// no host synchronisation, and exists twice:
+//   NCCL  -- all-reduce / send-recv / broadcast on the context's stream;
+//   group -- peer copies between the contexts' streams ordered by events, values
+//            combined on the lead context in rank order (deterministic), ghost
+//            planes pulled from the neighbours' owned planes.
+// REPLICA-mode sums (the reference's threads == 1 order, parallel.hpp:22-24) are
+// chained across the slabs in rank order, so a split run stays bit-identical to
+// the single domain; FAST sums are per-slab trees plus one reduction.
+namespace {
+
+struct Team {
+    petto_ctx** c;
+    int n;
+    petto_ctx* lead() const { return c[0]; }
+    bool nccl() const { return n == 1 && c[0]->nccl_comm != nullptr; }
+    bool split() const { return n > 1 || nccl(); }
+    bool replica() const { return c[0]->mode == PETTO_MODE_REPLICA; }
+};
+
+using PtrOf = std::function<void*(petto_ctx*)>;
+using DblOf = std::function<double*(petto_ctx*)>;
+
+bool is_slab(const petto_ctx* ctx) { return ctx->g.kb != 0 || ctx->g.ke != ctx->g.nz; }
+
+// A context used on its own: a slab needs its communicator for the collectives.
+int solo_ok(petto_ctx* ctx, bool solve_only) {
+    if (ctx->nb_lo || ctx->nb_hi)
+        return fail(ctx, PETTO_INVALID, "slab context is linked in a local group: use the petto_dev_group_* calls");
+    if (is_slab(ctx) && !ctx->nccl_comm && !(solve_only && ctx->peer_halo))
+        return fail(ctx, PETTO_INVALID, "slab context without a communicator (petto_dev_comm_init)");
+    return PETTO_OK;
+}
+
+int team_check(Team t) {
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        if (t.n > 1 && (ctx->nb_lo != (i ? t.c[i - 1] : nullptr) || ctx->nb_hi != (i + 1 < t.n ? t.c[i + 1] : nullptr)))
+            return fail(ctx, PETTO_INVALID, "group: call petto_dev_group_link first");
+        if (ctx->mode != t.lead()->mode) return fail(ctx, PETTO_INVALID, "group: contexts differ in mode");
     }
     return PETTO_OK;
 }
 
-int petto_dev_design_update(petto_ctx* ctx) {
+// every stream of the group waits until every other one reached this point
+int team_sync(Team t) {
+    if (t.n == 1) return PETTO_OK;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaEventRecord(ctx->ev_team, ctx->stream));
+    }
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        for (int j = 0; j < t.n; ++j)
+            if (j != i) CK(cudaStreamWaitEvent(ctx->stream, t.c[j]->ev_team, 0));
+    }
+    return PETTO_OK;
+}
+
+enum { RED_SUM = 0, RED_MAX = 1, RED_MIN_I64 = 2, RED_SUM_U64 = 3, RED_MAX_U32 = 4 };
+constexpr int TEAM_MAX = 64;
+
+// in-place reduction of `count` device values at at(ctx) over the slabs
+int team_reduce(Team t, const PtrOf& at, int count, int op) {
+    const size_t es = op == RED_MAX_U32 ? 4 : 8;
+    if (t.n == 1) {
+        petto_ctx* ctx = t.c[0];
+        static const ncclDataType_t ty[5] = {ncclDouble, ncclDouble, ncclInt64, ncclUint64, ncclUint32};
+        static const ncclRedOp_t ro[5] = {ncclSum, ncclMax, ncclMin, ncclSum, ncclMax};
+        return allreduce(ctx, at(ctx), (size_t)count, ty[op], ro[op]);
+    }
+    petto_ctx* ctx = t.lead();
+    if (count > TEAM_MAX || t.n > TEAM_MAX) return fail(ctx, PETTO_INVALID, "group: too many slabs or values");
     CK(cudaSetDevice(ctx->device));
-    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
-    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
-    const Geo& g = ctx->g;
+    if (!ctx->team_buf) CK(cudaMalloc(&ctx->team_buf, 8 * TEAM_MAX * TEAM_MAX));
+    if (int rc = team_sync(t)) return rc;
+    CK(cudaSetDevice(ctx->device));
+    for (int i = 0; i < t.n; ++i)
+        CK(cudaMemcpyAsync(static_cast<char*>(ctx->team_buf) + (size_t)i * count * es, at(t.c[i]), count * es,
+                           cudaMemcpyDefault, ctx->stream));
+    k_team_combine<<<1, TEAM_MAX, 0, ctx->stream>>>(ctx->team_buf, t.n, count, op, at(ctx));
+    ctx->launches++;
+    CKL();
+    if (int rc = team_sync(t)) return rc;
+    for (int i = 1; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        if (cudaMemcpyAsync(at(x), at(ctx), count * es, cudaMemcpyDefault, x->stream) != cudaSuccess)
+            return fail(x, PETTO_ERROR, "group: reduction broadcast failed");
+    }
+    return team_sync(t);  // the lead may overwrite its value only after every copy
+}
+
+// Ordered sum over the slabs: segment s of every slab in rank order, s = 0..nseg-1
+// (the components of a vector field are segments: entry order c*N + node).
+// seg(ctx, s, init, out) launches one segment on ctx's stream continuing from
+// *init (nullptr: from zero).  The total lands in dst(ctx) of every context.
+using SegFn = std::function<int(petto_ctx*, int, const double*, double*)>;
+
+int team_chain(Team t, int nseg, const SegFn& seg, const DblOf& dst) {
+    petto_ctx* ctx = t.lead();
+    const bool ranks = t.nccl() && ctx->nranks > 1;
+    if (t.n == 1 && !ranks) {
+        for (int s = 0; s < nseg; ++s)
+            if (int rc = seg(ctx, s, s ? ctx->dscal + DS_CHAIN : nullptr, ctx->dscal + DS_CHAIN)) return rc;
+        CK(cudaMemcpyAsync(dst(ctx), ctx->dscal + DS_CHAIN, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return PETTO_OK;
+    }
+    if (ranks) {
+        NcclApi& N = nccl();
+        const ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+        const int r = ctx->rank, R = ctx->nranks;
+        for (int s = 0; s < nseg; ++s) {
+            const bool has_prev = r > 0 || s > 0, has_next = !(s == nseg - 1 && r == R - 1);
+            if (has_prev)
+                if (int rc = nccl_check(ctx, N.Recv(ctx->dscal + DS_CHAIN_IN, 1, ncclDouble, (r + R - 1) % R, comm,
+                                                    ctx->stream), "chain recv"))
+                    return rc;
+            if (int rc = seg(ctx, s, has_prev ? ctx->dscal + DS_CHAIN_IN : nullptr, ctx->dscal + DS_CHAIN)) return rc;
+            if (has_next)
+                if (int rc = nccl_check(ctx, N.Send(ctx->dscal + DS_CHAIN, 1, ncclDouble, (r + 1) % R, comm,
+                                                    ctx->stream), "chain send"))
+                    return rc;
+        }
+        if (int rc = nccl_check(ctx, N.Broadcast(ctx->dscal + DS_CHAIN, ctx->dscal + DS_CHAIN, 1, ncclDouble, R - 1,
+                                                 comm, ctx->stream), "chain broadcast"))
+            return rc;
+        CK(cudaMemcpyAsync(dst(ctx), ctx->dscal + DS_CHAIN, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return PETTO_OK;
+    }
+    if (int rc = team_sync(t)) return rc;
+    petto_ctx* before = nullptr;
+    for (int s = 0; s < nseg; ++s)
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            if (before) {
+                if (cudaStreamWaitEvent(x->stream, before->ev_team, 0) != cudaSuccess ||
+                    cudaMemcpyAsync(x->dscal + DS_CHAIN_IN, before->dscal + DS_CHAIN, 8, cudaMemcpyDefault,
+                                    x->stream) != cudaSuccess)
+                    return fail(x, PETTO_ERROR, "group: chain hand-off failed");
+            }
+            if (int rc = seg(x, s, before ? x->dscal + DS_CHAIN_IN : nullptr, x->dscal + DS_CHAIN)) return rc;
+            if (cudaEventRecord(x->ev_team, x->stream) != cudaSuccess)
+                return fail(x, PETTO_ERROR, "group: chain event failed");
+            before = x;
+        }
+    if (int rc = team_sync(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        if (cudaMemcpyAsync(dst(x), before->dscal + DS_CHAIN, 8, cudaMemcpyDefault, x->stream) != cudaSuccess)
+            return fail(x, PETTO_ERROR, "group: chain broadcast failed");
+    }
+    return team_sync(t);
+}
+
+// Sum over all slabs of the per-node terms every context left in term(ctx)[0,
+// len(ctx)) (owned nodes in k, j, i order, or region-list order), into dst(ctx).
+int team_sum_terms(Team t, const DblOf& term, const std::function<long long(petto_ctx*)>& len, const DblOf& dst) {
+    if (t.replica())
+        return team_chain(
+            t, 1,
+            [&](petto_ctx* ctx, int, const double* init, double* out) {
+                k_sum_serial<<<1, 32, 0, ctx->stream>>>(term(ctx), len(ctx), out, init);
+                ctx->launches++;
+                CKL();
+                return PETTO_OK;
+            },
+            dst);
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        const long long n = len(ctx);
+        const int nb = (int)std::min<long long>(ctx->npartials, blocks_for(n));
+        k_sum_partials<<<nb, 256, 0, ctx->stream>>>(term(ctx), n, ctx->partials);
+        k_sum_finish<<<1, 256, 0, ctx->stream>>>(ctx->partials, nb, dst(ctx));
+        ctx->launches += 2;
+        CKL();
+    }
+    return team_reduce(t, [&](petto_ctx* x) -> void* { return dst(x); }, 1, RED_SUM);
+}
+
+// Ghost planes of `comps` fields starting at f(ctx) (component stride Ns).
+int team_halo(Team t, const DblOf& f, int comps) {
+    if (t.n == 1) return t.nccl() ? halo_ptr(t.lead(), f(t.lead()), comps) : PETTO_OK;
+    if (int rc = team_sync(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        const Geo& g = ctx->g;
+        const size_t bytes = sizeof(double) * (size_t)g.px * g.ny;
+        for (petto_ctx* nb : {ctx->nb_lo, ctx->nb_hi}) {
+            if (!nb) continue;
+            const int k = nb == ctx->nb_lo ? g.kb - 1 : g.ke;
+            for (int c = 0; c < comps; ++c)
+                CK(cudaMemcpyAsync(f(ctx) + c * g.Ns + lidx(g, 0, 0, k), f(nb) + c * nb->g.Ns + lidx(nb->g, 0, 0, k),
+                                   bytes, cudaMemcpyDefault, ctx->stream));
+        }
+    }
+    return team_sync(t);
+}
+
+int team_phase_ghosts(Team t) {
+    bool stale = false;
+    for (int i = 0; i < t.n; ++i) stale |= t.c[i]->phi_ghosts_stale;
+    if (stale && t.split())
+        if (int rc = team_halo(t, [](petto_ctx* x) { return x->phases; }, t.lead()->mat.nphases)) return rc;
+    for (int i = 0; i < t.n; ++i) t.c[i]->phi_ghosts_stale = false;
+    return PETTO_OK;
+}
+
+// ------------------------------------------------------------ state solver
+
+int team_hybrid_solve(Team t, const petto_pt_params* p, int64_t* abort_step) {
+    if (int rc = team_check(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        if (int rc = validate_params(ctx, p)) return rc;
+        if (int rc = require_ready(ctx)) return rc;
+        if (int rc = check_kappa(ctx)) return rc;
+        if (int rc = reset_status(ctx)) return rc;
+    }
+    petto_ctx* ctx = t.lead();
+    const long long nsteps = p->n_apt + p->n_pt;
+    const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
+    const StepCoef kp = coef(2, p->dt_pt, p->theta);
+    auto first_bad = [](petto_ctx* x) -> void* { return &x->status->first_bad; };
+    if (t.n == 1 && small_solve_ok(ctx)) {
+        if (int rc = small_solve(ctx, ka, kp, p->n_apt, p->n_pt)) return rc;
+        if (nsteps % 2) std::swap(ctx->cur, ctx->prev);  // the kernel swapped nsteps times
+    } else {
+        for (long long step = 1; step <= nsteps; ++step) {
+            const StepCoef& k = step <= p->n_apt ? ka : kp;
+            if (t.n == 1 || use_peer(ctx)) {
+                // one context (its halo, peer or NCCL, inside), or a group whose fused
+                // steps store their boundary planes into the neighbours' ghosts
+                for (int i = 0; i < t.n; ++i) {
+                    CK(cudaSetDevice(t.c[i]->device));
+                    if (int rc = hybrid_step(t.c[i], k, step, nsteps)) return rc;
+                }
+            } else {
+                // group, other kernels: step every slab, then pull the ghost planes
+                for (int i = 0; i < t.n; ++i) {
+                    petto_ctx* x = t.c[i];
+                    CK(cudaSetDevice(x->device));
+                    // the buffer written now was read by the neighbours' pulls of the last step
+                    for (petto_ctx* nb : {x->nb_lo, x->nb_hi})
+                        if (nb) CK(cudaStreamWaitEvent(x->stream, nb->ev_pull, 0));
+                    if (int rc = state_step(x, k, x->cur, x->prev, x->st[x->prev], step, nsteps, false)) return rc;
+                    std::swap(x->cur, x->prev);
+                    CK(cudaEventRecord(x->ev_step, x->stream));
+                }
+                for (int i = 0; i < t.n; ++i) {
+                    CK(cudaSetDevice(t.c[i]->device));
+                    if (int rc = group_pull(t.c[i], t.c[i]->cur)) return rc;
+                }
+            }
+            // check_finite cadence (state_solver.hpp:490): every slab learns the
+            // first non-finite step of any slab at each check, so all skip alike
+            if (t.split() && step % 100 == 0 && step < nsteps)
+                if (int rc = team_reduce(t, first_bad, 1, RED_MIN_I64)) return rc;
+        }
+    }
+    if (int rc = team_reduce(t, first_bad, 1, RED_MIN_I64)) return rc;
+    long long fb = PETTO_NO_BAD;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        if (int rc = read_status(x)) return rc;
+        fb = std::min(fb, x->status_h->first_bad);
+    }
+    if (fb != PETTO_NO_BAD) {
+        const long long at = std::min(((fb + 99) / 100) * 100, nsteps);
+        // the kernels after `at` were skipped: the buffers still hold the state of
+        // step `at`, but the cur/prev indices advanced past it -- rewind the swaps
+        const std::string msg = "numerical abort in 'state' at step " + std::to_string(at) +
+                                ": non-finite values (time step too large?)";
+        for (int i = 0; i < t.n; ++i) {
+            if ((nsteps - at) % 2) std::swap(t.c[i]->cur, t.c[i]->prev);
+            fail(t.c[i], PETTO_ABORT, msg);
+        }
+        if (abort_step) *abort_step = at;
+        return PETTO_ABORT;
+    }
+    return PETTO_OK;
+}
+
+// residual + residual_norm (state_solver.hpp:49-58, 327-385): sqrt(sum r^2) / N
+int team_residual(Team t, double* r_pde) {
+    if (int rc = team_check(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        if (int rc = require_ready(ctx)) return rc;
+        if (int rc = check_kappa(ctx)) return rc;
+        if (int rc = reset_status(ctx)) return rc;
+        const StepCoef k = coef(3, 0.0, 1.0);
+        if (int rc = state_step(ctx, k, ctx->cur, ctx->prev, ctx->r, 0, 0, !t.replica())) return rc;
+        if (!t.replica()) {
+            k_sum_to<<<1, 256, 0, ctx->stream>>>(ctx->partials, ctx->npartials_used, &ctx->status->sumsq);
+            ctx->launches++;
+            CKL();
+        }
+    }
+    auto sumsq = [](petto_ctx* x) -> double* { return &x->status->sumsq; };
+    if (t.replica()) {
+        // entry order c*N + node: component after component, each over the slabs
+        if (int rc = team_chain(
+                t, t.lead()->comps,
+                [](petto_ctx* ctx, int c, const double* init, double* out) {
+                    k_sumsq_serial<<<1, 32, 0, ctx->stream>>>(ctx->g, ctx->comps, ctx->r, out, c, init);
+                    ctx->launches++;
+                    CKL();
+                    return PETTO_OK;
+                },
+                sumsq))
+            return rc;
+    } else if (int rc = team_reduce(t, [&](petto_ctx* x) -> void* { return sumsq(x); }, 1, RED_SUM)) {
+        return rc;
+    }
+    petto_ctx* ctx = t.lead();
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = read_status(ctx)) return rc;
+    if (r_pde) *r_pde = std::sqrt(ctx->status_h->sumsq) / (double)global_nodes(ctx);
+    return PETTO_OK;
+}
+
+// ------------------------------------------------------------ design loop
+
+int team_require_design(Team t, bool need_state) {
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+        if (need_state && !ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
+    }
+    return team_check(t);
+}
+
+long long owned_of(petto_ctx* x) { return owned_nodes(x); }
+
+// phase_mass per phase (phase_field.hpp:83-102) into dscal[slot + q]
+int team_phase_masses(Team t, int slot) {
+    for (int q = 0; q < t.lead()->mat.nphases; ++q) {
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* ctx = t.c[i];
+            CK(cudaSetDevice(ctx->device));
+            k_term_mass<<<blocks_for(owned_nodes(ctx)), 256, 0, ctx->stream>>>(ctx->g, ctx->phases + q * ctx->g.Ns,
+                                                                               ctx->term1);
+            ctx->launches++;
+            CKL();
+        }
+        if (int rc = team_sum_terms(t, [](petto_ctx* x) { return x->term1; }, owned_of,
+                                    [&](petto_ctx* x) { return x->dscal + slot + q; }))
+            return rc;
+    }
+    return PETTO_OK;
+}
+
+// region volume and per-phase region masses (objectives.hpp:251-288), list order
+int team_region_sums(Team t) {
+    if (!t.lead()->tgt.has_region) return PETTO_OK;
+    auto len = [](petto_ctx* x) { return (long long)x->region_nodes.size(); };
+    for (int q = -1; q < t.lead()->mat.nphases; ++q) {
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* ctx = t.c[i];
+            CK(cudaSetDevice(ctx->device));
+            k_region_terms<<<blocks_for(len(ctx)), 256, 0, ctx->stream>>>(
+                ctx->g, ctx->region_dev, len(ctx), q < 0 ? nullptr : ctx->phases + q * ctx->g.Ns, ctx->term1);
+            ctx->launches++;
+            CKL();
+        }
+        if (int rc = team_sum_terms(t, [](petto_ctx* x) { return x->term1; }, len,
+                                    [&](petto_ctx* x) { return x->dscal + (q < 0 ? DS_RVOL : DS_RACC + q); }))
+            return rc;
+    }
+    return PETTO_OK;
+}
+
+// interpolate_into (objectives.hpp:95-116) over every stored plane (the ghost
+// planes too: the operator reads the property of the cells across a slab face)
+int team_interpolate(Team t) {
+    if (int rc = team_require_design(t, false)) return rc;
+    if (int rc = team_phase_ghosts(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        const long long n = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nzs;
+        k_interpolate<<<blocks_for(n), 256, 0, ctx->stream>>>(ctx->g, design_params(ctx), ctx->phases, ctx->prop);
+        ctx->launches++;
+        CKL();
+        ctx->ecell_valid = false;
+        ctx->prop_node0_valid = false;
+        ctx->prop_is_mu = false;
+    }
+    return PETTO_OK;
+}
+
+// The elasticity operator's nu comes from node 0's Lame pair (state_solver.hpp:
+// 299-301); node 0 lives on the first slab, whose value every slab takes.
+int team_init_operator(Team t) {
+    petto_ctx* ctx = t.lead();
+    if (ctx->desc.physics == 1) {
+        double e0 = 0.0;
+        CK(cudaSetDevice(ctx->device));
+        if (t.nccl() && ctx->nranks > 1) {
+            if (ctx->rank == 0)
+                CK(cudaMemcpyAsync(ctx->dscal + DS_CHAIN_IN, ctx->prop + lidx(ctx->g, 0, 0, 0), 8,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+            if (int rc = nccl_check(ctx, nccl().Broadcast(ctx->dscal + DS_CHAIN_IN, ctx->dscal + DS_CHAIN_IN, 1,
+                                                          ncclDouble, 0, static_cast<ncclComm_t>(ctx->nccl_comm),
+                                                          ctx->stream), "node-0 broadcast"))
+                return rc;
+            CK(cudaMemcpyAsync(&e0, ctx->dscal + DS_CHAIN_IN, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        } else {
+            CK(cudaMemcpyAsync(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), 8, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < t.n; ++i) {
+            t.c[i]->prop_node0 = e0;
+            t.c[i]->prop_node0_valid = true;
+        }
+    }
+    for (int i = 0; i < t.n; ++i)
+        if (int rc = petto_dev_init_operator(t.c[i])) return rc;
+    return PETTO_OK;
+}
+
+// sensitivities (objectives.hpp:336-439) + design_update_inplace (:444-480)
+int team_design_update(Team t) {
+    if (int rc = team_require_design(t, true)) return rc;
+    petto_ctx* ctx = t.lead();
     const DesignP d = design_params(ctx);
-    if (int rc = phase_masses(ctx, DS_MASS)) return rc;  // volume_fractions of the pre-update design
-    if (int rc = region_sums(ctx)) return rc;
+    if (int rc = team_phase_masses(t, DS_MASS)) return rc;  // volume_fractions of the pre-update design
+    if (int rc = team_region_sums(t)) return rc;
     const double nu = ctx->mat.poisson_ratio;
     const double ctr = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     const double cec = 1.0 / (1.0 + nu);
-    const long long owned = owned_nodes(ctx);
-    const int nb = (int)std::min<long long>(ctx->npartials, blocks_for(owned));
-    k_sens_gc<<<nb, 256, 0, ctx->stream>>>(g, d, ctx->mat.kind, ctr, cec, ctx->phases, ctx->st[ctx->cur], ctx->gc,
-                                          ctx->pmax);
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        const int nb = (int)std::min<long long>(x->npartials, blocks_for(owned_nodes(x)));
+        k_sens_gc<<<nb, 256, 0, x->stream>>>(x->g, d, x->mat.kind, ctr, cec, x->phases, x->st[x->cur], x->gc,
+                                             x->pmax);
+        k_local_gmax<<<1, 32, 0, x->stream>>>(d.np, x->pmax, nb, x->dscal);
+        x->launches += 2;
+        if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "sensitivity launch failed");
+    }
+    // max_abs_nodes over the whole grid (parallel.hpp:33-42, objectives.hpp:459-461)
+    if (int rc = team_reduce(t, [](petto_ctx* x) -> void* { return x->dscal + DS_GMAX; }, d.np, RED_MAX)) return rc;
     UpdateScal u{};
     u.inv_vol = 1.0 / domain_volume(ctx);
     for (int q = 0; q < d.np; ++q) {
@@ -1622,41 +1955,71 @@ int petto_dev_design_update(petto_ctx* ctx) {
     u.alpha_r = ctx->wts.alpha_region;
     u.normalize = ctx->wts.normalize_compliance;
     u.sign = ctx->wts.compliance_sign;
-    k_design_scalars<<<1, 32, 0, ctx->stream>>>(d.np, u, ctx->dscal, ctx->pmax, nb);
-    k_design_update<<<blocks_for(owned), 256, 0, ctx->stream>>>(g, d.np, u, ctx->dscal, ctx->gc, ctx->region_mask,
-                                                               ctx->phases);
-    ctx->launches += 3;
-    CKL();
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        k_design_scalars<<<1, 32, 0, x->stream>>>(d.np, u, x->dscal);
+        k_design_update<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, d.np, u, x->dscal, x->gc,
+                                                                           x->region_mask, x->phases);
+        x->launches += 2;
+        if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "design update launch failed");
+        x->phi_ghosts_stale = true;
+    }
     return PETTO_OK;
 }
 
-int petto_dev_ch_step(petto_ctx* ctx, const petto_ch_params* p, petto_ch_stats* stats) {
-    CK(cudaSetDevice(ctx->device));
-    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+// ch_step_multi_inplace (phase_field.hpp:136-176): per phase, mass before, mu on
+// the owned planes from phi with fresh ghosts, phi += dt D lap(mu) with fresh mu
+// ghosts (the 2-plane footprint as two 1-plane exchanges), mass pre, clamp, mass post
+int team_ch_step(Team t, const petto_ch_params* p, petto_ch_stats* stats) {
+    if (int rc = team_require_design(t, false)) return rc;
+    petto_ctx* ctx = t.lead();
     // CahnHilliardParams::validate (phase_field.hpp:17-21)
     if (!(p->mobility > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: mobility must be positive");
     if (!(p->gamma > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: gamma must be positive");
     if (!(p->dt > 0.0)) return fail(ctx, PETTO_INVALID, "cahn-hilliard: dt must be positive");
-    const Geo& g = ctx->g;
-    const long long owned = owned_nodes(ctx);
-    const int nb = blocks_for(owned);
     const double step = p->dt * p->mobility;
+    auto term1 = [](petto_ctx* x) { return x->term1; };
     for (int q = 0; q < ctx->mat.nphases; ++q) {
-        double* phi = ctx->phases + q * g.Ns;
-        k_term_mass<<<nb, 256, 0, ctx->stream>>>(g, phi, ctx->term1);
-        ctx->launches++;
-        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q)) return rc;
-        k_chem_potential<<<nb, 256, 0, ctx->stream>>>(g, phi, p->gamma, ctx->scratch1);
-        k_ch_update<<<nb, 256, 0, ctx->stream>>>(g, ctx->scratch1, step, phi, ctx->term1);
-        ctx->launches += 2;
-        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q + 1)) return rc;
-        k_ch_clamp<<<nb, 256, 0, ctx->stream>>>(g, phi, ctx->term1, &ctx->status->flags);
-        ctx->launches++;
-        if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_CH + 3 * q + 2)) return rc;
+        auto phi = [q](petto_ctx* x) { return x->phases + q * x->g.Ns; };
+        auto slot = [q](int k) { return [q, k](petto_ctx* x) { return x->dscal + DS_CH + 3 * q + k; }; };
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            k_term_mass<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, phi(x), x->term1);
+            x->launches++;
+        }
+        if (int rc = team_sum_terms(t, term1, owned_of, slot(0))) return rc;
+        if (t.split())
+            if (int rc = team_halo(t, phi, 1)) return rc;
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            k_chem_potential<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, phi(x), p->gamma, x->scratch1);
+            x->launches++;
+        }
+        if (t.split())
+            if (int rc = team_halo(t, [](petto_ctx* x) { return x->scratch1; }, 1)) return rc;
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            k_ch_update<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, x->scratch1, step, phi(x), x->term1);
+            x->launches++;
+        }
+        if (int rc = team_sum_terms(t, term1, owned_of, slot(1))) return rc;
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            k_ch_clamp<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, phi(x), x->term1, &x->status->flags);
+            x->launches++;
+            if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "cahn-hilliard launch failed");
+        }
+        if (int rc = team_sum_terms(t, term1, owned_of, slot(2))) return rc;
     }
-    CKL();
+    for (int i = 0; i < t.n; ++i) t.c[i]->phi_ghosts_stale = true;
     if (stats) {
         double h[3 * PETTO_MAX_PHASES];
+        CK(cudaSetDevice(ctx->device));
         CK(cudaMemcpyAsync(h, ctx->dscal + DS_CH, sizeof(double) * 3 * ctx->mat.nphases, cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1669,32 +2032,40 @@ int petto_dev_ch_step(petto_ctx* ctx, const petto_ch_params* p, petto_ch_stats* 
     return PETTO_OK;
 }
 
-int petto_dev_objectives(petto_ctx* ctx, petto_report* rep, double* separation) {
-    CK(cudaSetDevice(ctx->device));
-    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
-    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
-    const Geo& g = ctx->g;
+// evaluate_objectives (objectives.hpp:304-320) + the separation metric
+// (optimizer.hpp:95-112) of the current design and state
+int team_objectives(Team t, petto_report* rep, double* separation) {
+    if (int rc = team_require_design(t, true)) return rc;
+    petto_ctx* ctx = t.lead();
     const int np = ctx->mat.nphases;
-    const long long owned = owned_nodes(ctx);
     const double nu = ctx->mat.poisson_ratio;
     const double cl = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     const double cm = 1.0 / (2.0 * (1.0 + nu));
-    CK(cudaMemsetAsync(ctx->count, 0, sizeof(unsigned long long), ctx->stream));
-    k_objective_terms<<<blocks_for(owned), 256, 0, ctx->stream>>>(g, design_params(ctx), ctx->mat.kind, cl, cm,
-                                                                 ctx->phases, ctx->st[ctx->cur], ctx->term1,
-                                                                 ctx->term2, ctx->count);
-    ctx->launches++;
-    CKL();
-    if (int rc = sum_terms(ctx, ctx->term1, owned, ctx->dscal + DS_OBJ)) return rc;
-    if (int rc = sum_terms(ctx, ctx->term2, owned, ctx->dscal + DS_OBJ + 1)) return rc;
-    if (int rc = phase_masses(ctx, DS_TMP)) return rc;
-    if (int rc = region_sums(ctx)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* x = t.c[i];
+        CK(cudaSetDevice(x->device));
+        CK(cudaMemsetAsync(x->count, 0, sizeof(unsigned long long), x->stream));
+        k_objective_terms<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(
+            x->g, design_params(x), x->mat.kind, cl, cm, x->phases, x->st[x->cur], x->term1, x->term2, x->count);
+        x->launches++;
+        if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "objective launch failed");
+    }
+    if (int rc = team_sum_terms(t, [](petto_ctx* x) { return x->term1; }, owned_of,
+                                [](petto_ctx* x) { return x->dscal + DS_OBJ; }))
+        return rc;
+    if (int rc = team_sum_terms(t, [](petto_ctx* x) { return x->term2; }, owned_of,
+                                [](petto_ctx* x) { return x->dscal + DS_OBJ + 1; }))
+        return rc;
+    if (int rc = team_reduce(t, [](petto_ctx* x) -> void* { return x->count; }, 1, RED_SUM_U64)) return rc;
+    if (int rc = team_phase_masses(t, DS_TMP)) return rc;
+    if (int rc = team_region_sums(t)) return rc;
     double h[DS_COUNT];
     unsigned long long cnt = 0;
+    CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(h, ctx->dscal, sizeof(double) * DS_COUNT, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&cnt, ctx->count, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    // evaluate_objectives (objectives.hpp:304-320), scalar parts on the host
+    // scalar parts on the host, as the reference forms them
     const double inv_vol = 1.0 / domain_volume(ctx);
     petto_report r{};
     r.compliance = h[DS_OBJ];
@@ -1722,8 +2093,8 @@ int petto_dev_objectives(petto_ctx* ctx, petto_report* rep, double* separation) 
 
 // run() (optimizer.hpp:120-223): the coupled loop with every field resident in HBM;
 // the host only sees scalars (records, CH mass stats, abort flags).
-int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, void* user,
-                  petto_run_result* result) {
+int team_run(Team t, const petto_schedule* s, petto_record_cb cb, void* user, petto_run_result* result) {
+    petto_ctx* ctx = t.lead();
     CK(cudaSetDevice(ctx->device));
     // LoopSchedule::validate (optimizer.hpp:23-33)
     if (int rc = validate_params(ctx, &s->pt)) return rc;
@@ -1735,23 +2106,23 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
         return fail(ctx, PETTO_INVALID, "schedule: convergence tolerance must be positive");
     if (s->convergence_window < 2) return fail(ctx, PETTO_INVALID, "schedule: convergence window must be >= 2");
     if (s->report_every < 1) return fail(ctx, PETTO_INVALID, "schedule: report_every must be >= 1");
-    if (!ctx->design_set) return fail(ctx, PETTO_INVALID, "design not set (petto_dev_set_design)");
+    if (int rc = team_require_design(t, true)) return rc;
     if (int rc = validate_design(ctx, &ctx->mat, &ctx->wts)) return rc;
-    if (!ctx->state_set) return fail(ctx, PETTO_INVALID, "state not set");
 
     petto_run_result res{};
     // operator construction on the initial design (optimizer.hpp:131-138)
-    if (int rc = petto_dev_interpolate(ctx, nullptr)) return rc;
-    if (int rc = petto_dev_init_operator(ctx)) return rc;
+    if (int rc = team_interpolate(t)) return rc;
+    if (int rc = team_init_operator(t)) return rc;
     std::vector<double> comp_hist;
     const auto t0 = std::chrono::steady_clock::now();
     res.termination = 1;
     std::vector<petto_ch_stats> chs(ctx->mat.nphases);
+    auto flags = [](petto_ctx* x) -> void* { return &x->status->flags; };
     for (long loop = 1; loop <= s->max_loops; ++loop) {
         res.loops = loop;
-        if (int rc = petto_dev_interpolate(ctx, nullptr)) return rc;
+        if (int rc = team_interpolate(t)) return rc;
         int64_t astep = 0;
-        int rc = petto_dev_hybrid_solve(ctx, &s->pt, &astep);
+        int rc = team_hybrid_solve(t, &s->pt, &astep);
         if (rc == PETTO_ABORT) {
             res.termination = 2;
             std::snprintf(res.abort_detail, sizeof res.abort_detail, "loop %ld: %s", loop, ctx->err.c_str());
@@ -1760,12 +2131,19 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
         if (rc) return rc;
         res.apt_steps += s->pt.n_apt;
         res.pt_steps += s->pt.n_pt;
-        if ((rc = petto_dev_design_update(ctx))) return rc;
+        if ((rc = team_design_update(t))) return rc;
         ++res.design_updates;
-        CK(cudaMemsetAsync(&ctx->status->flags, 0, sizeof(unsigned), ctx->stream));
-        if ((rc = petto_dev_ch_step(ctx, &s->ch, chs.data()))) return rc;
+        for (int i = 0; i < t.n; ++i) {
+            petto_ctx* x = t.c[i];
+            CK(cudaSetDevice(x->device));
+            CK(cudaMemsetAsync(&x->status->flags, 0, sizeof(unsigned), x->stream));
+        }
+        if ((rc = team_ch_step(t, &s->ch, chs.data()))) return rc;
         ++res.ch_steps;
         for (const petto_ch_stats& st : chs) res.clamp_mass_drift += std::abs(st.mass_postclamp - st.mass_preclamp);
+        // all_finite of the phases (optimizer.hpp:203-205), any slab
+        if ((rc = team_reduce(t, flags, 1, RED_MAX_U32))) return rc;
+        CK(cudaSetDevice(ctx->device));
         if ((rc = read_status(ctx))) return rc;
         if (ctx->status_h->flags & 4u) {
             res.termination = 2;
@@ -1778,7 +2156,7 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
             petto_record rec{};
             petto_report rep{};
             double sep = 0.0;
-            if ((rc = petto_dev_objectives(ctx, &rep, &sep))) return rc;
+            if ((rc = team_objectives(t, &rep, &sep))) return rc;
             rec.loop = loop;
             rec.apt_steps = res.apt_steps;
             rec.pt_steps = res.pt_steps;
@@ -1788,8 +2166,8 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
             rec.region = rep.region;
             for (int q = 0; q < ctx->mat.nphases; ++q) rec.volume_fractions[q] = rep.volume_fractions[q];
             // the operator sees the property of the updated design (optimizer.hpp:157-162)
-            if ((rc = petto_dev_interpolate(ctx, nullptr))) return rc;
-            if ((rc = petto_dev_residual(ctx, nullptr, &rec.r_pde))) return rc;
+            if ((rc = team_interpolate(t))) return rc;
+            if ((rc = team_residual(t, &rec.r_pde))) return rc;
             rec.separation = sep;
             rec.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             comp_hist.push_back(rec.compliance);
@@ -1813,6 +2191,91 @@ int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, v
     }
     if (result) *result = res;
     return PETTO_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------- C-ABI over the teams
+
+int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* abort_step) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, true)) return rc;
+    return team_hybrid_solve(Team{&ctx, 1}, p, abort_step);
+}
+
+int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    if (int rc = team_residual(Team{&ctx, 1}, r_pde)) return rc;
+    if (out) {
+        if (int rc = download(ctx, out, ctx->r, ctx->comps)) return rc;
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_interpolate(petto_ctx* ctx, double* property_out) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    if (int rc = team_interpolate(Team{&ctx, 1})) return rc;
+    if (property_out) {
+        if (int rc = download(ctx, property_out, ctx->prop, 1)) return rc;
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return PETTO_OK;
+}
+
+int petto_dev_design_update(petto_ctx* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    return team_design_update(Team{&ctx, 1});
+}
+
+int petto_dev_ch_step(petto_ctx* ctx, const petto_ch_params* p, petto_ch_stats* stats) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    return team_ch_step(Team{&ctx, 1}, p, stats);
+}
+
+int petto_dev_objectives(petto_ctx* ctx, petto_report* rep, double* separation) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    return team_objectives(Team{&ctx, 1}, rep, separation);
+}
+
+int petto_dev_run(petto_ctx* ctx, const petto_schedule* s, petto_record_cb cb, void* user,
+                  petto_run_result* result) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    return team_run(Team{&ctx, 1}, s, cb, user, result);
+}
+
+int petto_dev_group_hybrid_solve(petto_ctx** c, int n, const petto_pt_params* p, int64_t* abort_step) {
+    return team_hybrid_solve(Team{c, n}, p, abort_step);
+}
+
+int petto_dev_group_residual(petto_ctx** c, int n, double* r_pde) { return team_residual(Team{c, n}, r_pde); }
+
+int petto_dev_group_interpolate(petto_ctx** c, int n) { return team_interpolate(Team{c, n}); }
+
+int petto_dev_group_init_operator(petto_ctx** c, int n) {
+    if (int rc = team_check(Team{c, n})) return rc;
+    return team_init_operator(Team{c, n});
+}
+
+int petto_dev_group_design_update(petto_ctx** c, int n) { return team_design_update(Team{c, n}); }
+
+int petto_dev_group_ch_step(petto_ctx** c, int n, const petto_ch_params* p, petto_ch_stats* stats) {
+    return team_ch_step(Team{c, n}, p, stats);
+}
+
+int petto_dev_group_objectives(petto_ctx** c, int n, petto_report* rep, double* separation) {
+    return team_objectives(Team{c, n}, rep, separation);
+}
+
+int petto_dev_group_run(petto_ctx** c, int n, const petto_schedule* s, petto_record_cb cb, void* user,
+                        petto_run_result* result) {
+    return team_run(Team{c, n}, s, cb, user, result);
 }
 
 // ------------------------------------------------------------ slab decomposition
@@ -1916,6 +2379,7 @@ int petto_dev_group_link(petto_ctx** c, int n) {
         CK(cudaSetDevice(x->device));
         if (!x->ev_step) CK(cudaEventCreateWithFlags(&x->ev_step, cudaEventDisableTiming));
         if (!x->ev_pull) CK(cudaEventCreateWithFlags(&x->ev_pull, cudaEventDisableTiming));
+        if (!x->ev_team) CK(cudaEventCreateWithFlags(&x->ev_team, cudaEventDisableTiming));
         CK(cudaEventRecord(x->ev_step, x->stream));
         CK(cudaEventRecord(x->ev_pull, x->stream));
         if (int rc = peer_prepare(x)) return rc;
@@ -1950,65 +2414,6 @@ int petto_dev_group_link(petto_ctx** c, int n) {
         fill(x->peer_hi, x->nb_hi, 0);
         x->peer_halo = n > 1;
         x->peer_seq = 0;
-    }
-    return PETTO_OK;
-}
-
-// hybrid_solve over a linked group: every step runs on all slabs.  Fused 3D steps
-// use the peer halo (boundary planes stored into the neighbours' ghosts, steps
-// ordered by stream flags); the other kernels pull the ghost planes afterwards
-// (stream-ordered copies, no host sync).
-int petto_dev_group_hybrid_solve(petto_ctx** c, int n, const petto_pt_params* p, int64_t* abort_step) {
-    petto_ctx* ctx = c[0];  // error sink of CK()
-    for (int i = 0; i < n; ++i) {
-        CK(cudaSetDevice(c[i]->device));
-        if (int rc = validate_params(c[i], p)) return rc;
-        if (int rc = require_ready(c[i])) return rc;
-        if (int rc = check_kappa(c[i])) return rc;
-        if (int rc = reset_status(c[i])) return rc;
-        if (n > 1 && (c[i]->nb_lo != (i ? c[i - 1] : nullptr) || c[i]->nb_hi != (i + 1 < n ? c[i + 1] : nullptr)))
-            return fail(c[i], PETTO_INVALID, "group: call petto_dev_group_link first");
-    }
-    const long long nsteps = p->n_apt + p->n_pt;
-    const StepCoef ka = coef(p->form ? 1 : 0, p->dt_apt, p->theta);
-    const StepCoef kp = coef(2, p->dt_pt, p->theta);
-    for (long long step = 1; step <= nsteps; ++step) {
-        const StepCoef& k = step <= p->n_apt ? ka : kp;
-        if (use_peer(c[0])) {
-            for (int i = 0; i < n; ++i) {
-                CK(cudaSetDevice(c[i]->device));
-                if (int rc = hybrid_step(c[i], k, step, nsteps)) return rc;
-            }
-            continue;
-        }
-        for (int i = 0; i < n; ++i) {
-            petto_ctx* x = c[i];
-            CK(cudaSetDevice(x->device));
-            // the buffer written now was read by the neighbours' pulls of the last step
-            for (petto_ctx* nb : {x->nb_lo, x->nb_hi})
-                if (nb) CK(cudaStreamWaitEvent(x->stream, nb->ev_pull, 0));
-            if (int rc = state_step(x, k, x->cur, x->prev, x->st[x->prev], step, nsteps, false)) return rc;
-            std::swap(x->cur, x->prev);
-            CK(cudaEventRecord(x->ev_step, x->stream));
-        }
-        for (int i = 0; i < n; ++i) {
-            CK(cudaSetDevice(c[i]->device));
-            if (int rc = group_pull(c[i], c[i]->cur)) return rc;
-        }
-    }
-    long long fb = PETTO_NO_BAD;
-    for (int i = 0; i < n; ++i) {
-        CK(cudaSetDevice(c[i]->device));
-        if (int rc = read_status(c[i])) return rc;
-        fb = std::min(fb, c[i]->status_h->first_bad);
-    }
-    if (fb != PETTO_NO_BAD) {
-        const long long at = std::min(((fb + 99) / 100) * 100, nsteps);
-        for (int i = 0; i < n; ++i)
-            if ((nsteps - at) % 2) std::swap(c[i]->cur, c[i]->prev);
-        if (abort_step) *abort_step = at;
-        return fail(c[0], PETTO_ABORT, "numerical abort in 'state' at step " + std::to_string(at) +
-                                           ": non-finite values (time step too large?)");
     }
     return PETTO_OK;
 }

@@ -153,11 +153,13 @@ __global__ void k_update_replica(Geo g, int comps, int form, const double* __res
 }
 
 // par::sum_nodes serial branch (parallel.hpp:22-24) of r^2 in entry order
-// (entry = c*N + node, node in k, j, i order): one thread, bit-exact.
-__global__ void k_sumsq_serial(Geo g, int comps, const double* __restrict__ r, double* out) {
+// (entry = c*N + node, node in k, j, i order): one thread, bit-exact.  With
+// c0 >= 0 only component c0, continuing from *init (the team chain over slabs).
+__global__ void k_sumsq_serial(Geo g, int comps, const double* __restrict__ r, double* out, int c0 = -1,
+                               const double* init = nullptr) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    double s = 0.0;
-    for (int c = 0; c < comps; ++c)
+    double s = init ? *init : 0.0;
+    for (int c = c0 < 0 ? 0 : c0; c < (c0 < 0 ? comps : c0 + 1); ++c)
         for (int k = g.kb; k < g.ke; ++k)
             for (int j = 0; j < g.ny; ++j) {
                 const double* row = r + c * g.Ns + lidx(g, 0, j, k);

@@ -148,7 +148,10 @@ EXPORTED = [
     "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
     "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
     "petto_dev_kernel_timing", "petto_dev_kernel_stats", "petto_dev_comm_unique_id", "petto_dev_comm_init",
-    "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_peer_export", "petto_dev_peer_import",
+    "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_group_residual", "petto_dev_group_interpolate",
+    "petto_dev_group_init_operator",
+    "petto_dev_group_design_update", "petto_dev_group_ch_step", "petto_dev_group_objectives", "petto_dev_group_run",
+    "petto_dev_peer_export", "petto_dev_peer_import",
     "petto_dev_write_field_csv", "petto_dev_write_vtk", "petto_dev_write_pgm", "petto_dev_format_values",
 ]
 
@@ -167,11 +170,53 @@ def group_link(ctxs):
     ctxs[0]._check(lib().petto_dev_group_link(arr, len(ctxs)))
 
 
+def _group(ctxs):
+    return (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+
+
 def group_hybrid_solve(ctxs, params):
     """hybrid_solve on a linked group of slab contexts (one process)."""
-    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
     step = C.c_int64(0)
-    ctxs[0]._check(lib().petto_dev_group_hybrid_solve(arr, len(ctxs), C.byref(pt_params(params)), C.byref(step)))
+    ctxs[0]._check(lib().petto_dev_group_hybrid_solve(_group(ctxs), len(ctxs), C.byref(pt_params(params)),
+                                                      C.byref(step)))
+
+
+def group_residual(ctxs):
+    """residual_norm of the whole decomposed grid (the residual stays on the slabs)."""
+    r = C.c_double(0.0)
+    ctxs[0]._check(lib().petto_dev_group_residual(_group(ctxs), len(ctxs), C.byref(r)))
+    return r.value
+
+
+def group_interpolate(ctxs):
+    ctxs[0]._check(lib().petto_dev_group_interpolate(_group(ctxs), len(ctxs)))
+
+
+def group_init_operator(ctxs):
+    ctxs[0]._check(lib().petto_dev_group_init_operator(_group(ctxs), len(ctxs)))
+
+
+def group_design_update(ctxs):
+    ctxs[0]._check(lib().petto_dev_group_design_update(_group(ctxs), len(ctxs)))
+
+
+def group_ch_step(ctxs, mobility, gamma, dt):
+    st = (CHStats * ctxs[0].nphases)()
+    ctxs[0]._check(lib().petto_dev_group_ch_step(_group(ctxs), len(ctxs), C.byref(CHParams(mobility, gamma, dt)), st))
+    return [(s.mass_before, s.mass_preclamp, s.mass_postclamp) for s in st]
+
+
+def group_objectives(ctxs):
+    rep = Report()
+    sep = C.c_double(0.0)
+    ctxs[0]._check(lib().petto_dev_group_objectives(_group(ctxs), len(ctxs), C.byref(rep), C.byref(sep)))
+    return rep, sep.value
+
+
+def group_run(ctxs, sched, callback=None):
+    """run() (optimizer.hpp:120-223) over a linked group of slab contexts."""
+    return ctxs[0]._run(sched, callback, lambda s, cb, res: lib().petto_dev_group_run(
+        _group(ctxs), len(ctxs), C.byref(s), cb, None, C.byref(res)))
 
 
 def _dp(a):
@@ -318,8 +363,9 @@ class Context:
     def set_phases(self, phases):
         self._check(lib().petto_dev_set_phases(self.h, _dp(_f64(phases))))
 
-    def get_phases(self):
-        out = np.zeros(self.nphases * self.N)
+    def get_phases(self, out=None):
+        """Download the phases (a slab fills its owned planes of `out`)."""
+        out = out if out is not None else np.zeros(self.nphases * self.N)
         self._check(lib().petto_dev_get_phases(self.h, _dp(out)))
         return out
 
@@ -344,6 +390,10 @@ class Context:
 
     def run(self, sched, callback=None):
         """run() (optimizer.hpp:120-223); returns (RunResult, [Record])."""
+        return self._run(sched, callback, lambda s, cb, res: lib().petto_dev_run(self.h, C.byref(s), cb, None,
+                                                                                 C.byref(res)))
+
+    def _run(self, sched, callback, call):
         s = Schedule(pt_params(sched.pt), CHParams(sched.ch_mobility, sched.ch_gamma, sched.dt_ch),
                      sched.max_loops, sched.convergence_tol, sched.convergence_window, sched.report_every)
         records = []
@@ -358,7 +408,7 @@ class Context:
 
         cb = RECORD_CB(_cb)
         res = RunResult()
-        self._check(lib().petto_dev_run(self.h, C.byref(s), cb, None, C.byref(res)))
+        self._check(call(s, cb, res))
         return res, records
 
     @staticmethod

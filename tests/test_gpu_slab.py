@@ -178,3 +178,166 @@ def test_peer_halo_multiprocess(nproc):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"peer halo, {nproc} processes: bit-identical" in r.stdout
 
+
+
+# --------------------------------------------------------------- design loop
+# The whole run() on slabs: ghost planes of phi and mu around the
+# Cahn-Hilliard kernels, every global scalar reduced over the slabs (REPLICA: one
+# serial sum chained across the slabs in order), node 0's Lame pair shared.
+
+
+def _slabs(prob, nranks, mode):
+    ctxs = [D.Context.from_problem(prob, mode, k_range=slab.slab_range(r, nranks, prob.grid.n[2]))
+            for r in range(nranks)]
+    D.group_link(ctxs)
+    return ctxs
+
+
+def _gather_phases(ctxs, prob):
+    out = np.full(prob.nphases * prob.grid.num_nodes, np.nan)
+    for c in ctxs:
+        c.get_phases(out)
+    return out
+
+
+RUN_SLAB_CASES = [
+    ("C4", dict(max_loops=3, report_every=1), [2, 3, 4]),                      # full C4 grid, 3 loops
+    ("drone3d", dict(nx=24, ny=12, nz=20, n_apt=20, n_pt=20, max_loops=3, report_every=1), [3]),  # heat + region
+]
+
+
+def _config(name, kw):
+    if name in P.CONFIGS:
+        return P.config(name, **kw)
+    cfg = P.make_preset(name)
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+@pytest.mark.parametrize("mode", [D.MODE_REPLICA, D.MODE_FAST])
+@pytest.mark.parametrize("case", range(len(RUN_SLAB_CASES)))
+def test_group_run_equals_single_domain(case, mode):
+    name, kw, splits = RUN_SLAB_CASES[case]
+    cfg = _config(name, kw)
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=D.spectral_bound)
+    one = D.Context.from_problem(prob, mode)
+    wres, wrecs = one.run(sched)
+    wph = one.get_phases()
+    wst = one.get_state()[0]
+    for nranks in splits:
+        ctxs = _slabs(prob, nranks, mode)
+        res, recs = D.group_run(ctxs, sched)
+        assert (res.loops, res.termination, res.apt_steps, res.pt_steps) == (
+            wres.loops, wres.termination, wres.apt_steps, wres.pt_steps)
+        ph = _gather_phases(ctxs, prob)
+        st = np.full(prob.comps * prob.grid.num_nodes, np.nan)
+        for c in ctxs:
+            c.get_state(st, None)
+        fields = ("compliance", "volume", "unity", "region", "r_pde", "separation")
+        if mode == D.MODE_REPLICA:
+            for a, b in zip(recs, wrecs):
+                assert [getattr(a, f) for f in fields] == [getattr(b, f) for f in fields]
+                assert list(a.volume_fractions) == list(b.volume_fractions)
+            assert np.array_equal(ph, wph) and np.array_equal(st, wst)
+            assert res.clamp_mass_drift == wres.clamp_mass_drift
+        else:
+            for a, b in zip(recs, wrecs):
+                for f in fields:
+                    x, y = getattr(a, f), getattr(b, f)
+                    assert abs(x - y) <= 1e-12 * max(abs(y), 1e-30), (nranks, f, x, y)
+            assert np.abs(ph - wph).max() <= 1e-12
+            assert np.abs(st - wst).max() <= 1e-12 * np.abs(wst).max()
+        del ctxs
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_group_design_calls_replica_bit_exact(nranks):
+    """design_update, ch_step, objectives and the residual norm of a split grid,
+    call by call, bit-identical to one domain (REPLICA)."""
+    cfg = P.config("C4", nx=40, ny=17, nz=14)
+    prob = P.build_problem(cfg)
+    g = prob.grid
+    sched = P.build_schedule(cfg, g, spectral_bound=D.spectral_bound)
+    state = H.random_field(3 * g.num_nodes, 8, -0.15, 0.15)
+    phases = H.rng(42).uniform(0.2, 0.8, prob.nphases * g.num_nodes)
+    one = D.Context.from_problem(prob, D.MODE_REPLICA)
+    ctxs = _slabs(prob, nranks, D.MODE_REPLICA)
+    for c in [one] + ctxs:
+        c.set_phases(phases)
+        c.set_state(state, state)
+    one.interpolate(download=False)
+    one.init_operator()
+    D.group_interpolate(ctxs)
+    D.group_init_operator(ctxs)
+    assert D.group_residual(ctxs) == one.residual()[1]
+    rep1, sep1 = one.objectives()
+    rep2, sep2 = D.group_objectives(ctxs)
+    assert (rep1.compliance, rep1.unity, rep1.volume, sep1) == (rep2.compliance, rep2.unity, rep2.volume, sep2)
+    one.design_update()
+    D.group_design_update(ctxs)
+    assert np.array_equal(_gather_phases(ctxs, prob), one.get_phases())
+    s1 = one.ch_step(sched.ch_mobility, sched.ch_gamma, sched.dt_ch)
+    s2 = D.group_ch_step(ctxs, sched.ch_mobility, sched.ch_gamma, sched.dt_ch)
+    assert s1 == s2
+    assert np.array_equal(_gather_phases(ctxs, prob), one.get_phases())
+
+
+def test_linked_slab_refuses_single_context_calls():
+    """A slab of a local group has no collectives of its own: the single-context
+    design / run / residual entry points refuse it instead of computing slab-local
+    sums (the group entry points are the way in)."""
+    cfg = P.config("C4", nx=24, ny=10, nz=12)
+    prob = P.build_problem(cfg)
+    sched = P.build_schedule(cfg, prob.grid, spectral_bound=D.spectral_bound)
+    ctxs = _slabs(prob, 2, D.MODE_FAST)
+    for call in (lambda c: c.run(sched), lambda c: c.design_update(), lambda c: c.objectives(),
+                 lambda c: c.ch_step(1.0, 3e-5, 1e-6), lambda c: c.residual()):
+        with pytest.raises(ValueError, match="group"):
+            call(ctxs[1])
+    lone = D.Context.from_problem(prob, D.MODE_FAST, k_range=(0, 6))  # a slab without a communicator
+    with pytest.raises(ValueError, match="communicator"):
+        lone.run(sched)
+
+
+@pytest.mark.parametrize("mode", [D.MODE_FAST, D.MODE_REPLICA])
+def test_group_abort_at_same_check_as_single_domain(mode):
+    """A non-finite value on the first slab spreads one plane per step and reaches
+    the last slab only after the first check_finite (step 100).  Every slab learns
+    the first non-finite step of any slab at each check, so all stop at step 100
+    like the single domain (without that reduction the last slab would run on to
+    step 200) and the state left behind is the single domain's state."""
+    g = P.Grid.make3d(16, 8, 240, 1.0, 0.5, 15.0)
+    comps, prop, src, bc, cur, prev = inputs(g, 1)
+    cur = cur.copy()
+    cur[g.node(0, 4, 2)] = np.nan
+    e, v = P.make_constraints(g, bc, comps)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.1 * h, theta=1.0, n_apt=0, n_pt=450, form=1)
+
+    def setup(ctx):
+        ctx.set_constraints(e, v)
+        ctx.set_source(src)
+        ctx.set_property(prop)
+        ctx.init_operator()
+        ctx.set_state(cur, prev)
+
+    one = D.Context(g, 1, 0.3, mode)
+    setup(one)
+    with pytest.raises(D.NumericalAbort) as ex1:
+        one.hybrid_solve(p)
+    want = one.get_state()[0]
+    ctxs = [D.Context(g, 1, 0.3, mode, k_range=slab.slab_range(r, 3, g.n[2])) for r in range(3)]
+    for c in ctxs:
+        setup(c)
+    D.group_link(ctxs)
+    with pytest.raises(D.NumericalAbort) as ex2:
+        D.group_hybrid_solve(ctxs, p)
+    assert ex1.value.step == ex2.value.step == 100
+    got = np.full(comps * g.num_nodes, np.nan)
+    for c in ctxs:
+        c.get_state(got, None)
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), fin) and 0 < fin.sum() < fin.size
+    assert np.array_equal(got[fin], want[fin])
