@@ -76,17 +76,35 @@ private:
 
 // A StateOperator whose residual runs on the B200.  residual() is the host-buffer
 // path (upload, evaluate, download); the solvers below keep the state resident.
+//
+// Like the reference operators (state_solver.hpp:91-94, 318-324), a DeviceOperator
+// aliases the caller's material field (kappa, or the Lame pair): the field must
+// outlive the operator, and every residual / hybrid_solve / iterate_to_tolerance
+// re-reads it, so a loop that updates the field in place between solves
+// (interpolate_into + update_lame, optimizer.hpp:187-189) is seen by the device.
+// The loads / source are read once, at construction (run() never changes them);
+// call refresh_loads() after changing them in place.  set_static_material(true)
+// skips the per-call material upload when the caller knows the field is fixed.
 class DeviceOperator : public StateOperator<double> {
 public:
     int components() const override { return comps_; }
     const ConstraintSet& constraints() const override { return cs_; }
     void residual(const Field<double>& state, Field<double>& out) const override {
         petto_ctx* c = ctx_->get();
+        refresh();
         check(c, petto_dev_set_state(c, state.data.data(), state.data.data()));
         double r = 0.0;
         check(c, petto_dev_residual(c, out.data.data(), &r));
     }
     petto_ctx* ctx() const { return ctx_->get(); }
+    // upload the aliased material field again (no-op with a static material)
+    void refresh() const {
+        if (!static_material_ && upload_material_) upload_material_();
+    }
+    void refresh_loads() const {
+        if (upload_loads_) upload_loads_();
+    }
+    void set_static_material(bool on) { static_material_ = on; }
 
 protected:
     DeviceOperator(const Grid& g, int physics, double nu, const BoundarySpec& bc, int mode)
@@ -99,6 +117,8 @@ protected:
     std::unique_ptr<Context> ctx_;
     int comps_;
     ConstraintSet cs_;
+    std::function<void()> upload_material_, upload_loads_;
+    bool static_material_ = false;
 };
 
 // HeatOperator (state_solver.hpp:76-95)
@@ -107,8 +127,12 @@ public:
     HeatOperator(const Grid& g, const Field<double>& kappa, const Field<double>& source, const BoundarySpec& bc,
                  int mode = PETTO_MODE_FAST)
         : DeviceOperator(g, 0, 0.3, bc, mode) {
-        check(ctx(), petto_dev_set_source(ctx(), source.data.data()));
-        check(ctx(), petto_dev_set_property(ctx(), kappa.data.data()));
+        const Field<double>* k = &kappa;
+        const Field<double>* f = &source;
+        upload_material_ = [this, k] { check(ctx(), petto_dev_set_property(ctx(), k->data.data())); };
+        upload_loads_ = [this, f] { check(ctx(), petto_dev_set_source(ctx(), f->data.data())); };
+        upload_loads_();
+        upload_material_();
         check(ctx(), petto_dev_init_operator(ctx()));
     }
 };
@@ -119,8 +143,14 @@ public:
     ElasticityOperator(const Grid& g, const ElasticMaterialField<double>& mat, const Field<double>& loads,
                        const BoundarySpec& bc, int mode = PETTO_MODE_FAST)
         : DeviceOperator(g, 1, nu_of(mat), bc, mode) {
-        check(ctx(), petto_dev_set_source(ctx(), loads.data.data()));
-        check(ctx(), petto_dev_set_lame(ctx(), mat.lambda.data.data(), mat.mu.data.data()));
+        const ElasticMaterialField<double>* m = &mat;
+        const Field<double>* f = &loads;
+        upload_material_ = [this, m] {
+            check(ctx(), petto_dev_set_lame(ctx(), m->lambda.data.data(), m->mu.data.data()));
+        };
+        upload_loads_ = [this, f] { check(ctx(), petto_dev_set_source(ctx(), f->data.data())); };
+        upload_loads_();
+        upload_material_();
         check(ctx(), petto_dev_init_operator(ctx()));
     }
 
@@ -138,6 +168,7 @@ inline petto_pt_params params(const PTParams& p) {
 // hybrid_solve (state_solver.hpp:480-498)
 inline void hybrid_solve(StateHistory<double>& hist, const DeviceOperator& op, const PTParams& p) {
     petto_ctx* c = op.ctx();
+    op.refresh();
     check(c, petto_dev_set_state(c, hist.current.data.data(), hist.previous.data.data()));
     const petto_pt_params pp = params(p);
     int64_t step = 0;
@@ -150,6 +181,7 @@ inline void hybrid_solve(StateHistory<double>& hist, const DeviceOperator& op, c
 inline SolveStats iterate_to_tolerance(StateHistory<double>& hist, const DeviceOperator& op, IterationMode mode,
                                        const PTParams& p, double target, long max_iters) {
     petto_ctx* c = op.ctx();
+    op.refresh();
     check(c, petto_dev_set_state(c, hist.current.data.data(), hist.previous.data.data()));
     const petto_pt_params pp = params(p);
     petto_solve_stats st{};

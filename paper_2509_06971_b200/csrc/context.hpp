@@ -49,6 +49,10 @@ struct petto_ctx {
     long long* cons_ent = nullptr; // device-local constrained entries (owned planes)
     double* cons_val = nullptr;
     long long ncons = 0;
+    std::vector<long long> cons_host;  // host copies: local constrained entries and their values,
+    std::vector<double> cons_vhost;    // and the local entries / values of the nonzero loads, so
+    std::vector<long long> load_host;  // aux and mask are rebuilt whatever the order of
+    std::vector<double> load_vhost;    // set_constraints and set_source
     double* r = nullptr;           // residual scratch
     double* Kdev = nullptr;        // unit-cell stiffness (replica)
     std::vector<double> K, kh;

@@ -968,22 +968,59 @@ int petto_dev_set_mode(petto_ctx* ctx, int mode) {
     return PETTO_OK;
 }
 
+// aux and mask from the context's constraint list and loads (whatever the order of
+// set_constraints / set_source): mask bit c = component c pinned, bit 3 = a load
+// at the node; aux = the pinned value at a constrained entry (apply_constraints,
+// grid.hpp:234-238), the load at the other entries.
+static int rebuild_aux_mask(petto_ctx* ctx) {
+    const Geo& g = ctx->g;
+    std::vector<unsigned char> hmask((size_t)g.Ns, 0);
+    std::vector<double> haux;
+    std::vector<long long> hidx;
+    for (long long le : ctx->cons_host) hmask[le % g.Ns] |= (unsigned char)(1u << (le / g.Ns));
+    for (size_t t = 0; t < ctx->load_host.size(); ++t) {
+        const long long le = ctx->load_host[t];
+        const long long node = le % g.Ns;
+        if (!((hmask[node] >> (le / g.Ns)) & 1u)) {
+            hidx.push_back(le);
+            haux.push_back(ctx->load_vhost[t]);
+        }
+    }
+    for (long long le : ctx->load_host) hmask[le % g.Ns] |= 8u;
+    hidx.insert(hidx.end(), ctx->cons_host.begin(), ctx->cons_host.end());
+    haux.insert(haux.end(), ctx->cons_vhost.begin(), ctx->cons_vhost.end());
+    CK(cudaMemcpyAsync(ctx->mask, hmask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->aux, 0, sizeof(double) * (size_t)g.Ns * ctx->comps, ctx->stream));
+    if (!hidx.empty()) {
+        long long* di = nullptr;
+        double* dv = nullptr;
+        CK(cudaMalloc(&di, sizeof(long long) * hidx.size()));
+        CK(cudaMalloc(&dv, sizeof(double) * haux.size()));
+        CK(cudaMemcpyAsync(di, hidx.data(), sizeof(long long) * hidx.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dv, haux.data(), sizeof(double) * haux.size(), cudaMemcpyHostToDevice, ctx->stream));
+        k_scatter_values<<<blocks_for((long long)hidx.size()), 256, 0, ctx->stream>>>(di, dv, (long long)hidx.size(),
+                                                                                      ctx->aux);
+        ctx->launches++;
+        CKL();
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(di);
+        cudaFree(dv);
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PETTO_OK;
+}
+
 int petto_dev_set_constraints(petto_ctx* ctx, const int64_t* entry, const double* value, int64_t count) {
     CK(cudaSetDevice(ctx->device));
-    const Geo& g = ctx->g;
     std::vector<long long> ent;
     std::vector<double> val;
-    std::unordered_map<long long, unsigned char> bits;
     for (int64_t t = 0; t < count; ++t) {
-        int c = 0;
-        long long node = 0;
-        const long long le = local_entry(ctx, entry[t], &c, &node);
         if (entry[t] < 0 || entry[t] >= global_nodes(ctx) * ctx->comps)
             return fail(ctx, PETTO_INVALID, "constraint entry outside the field");
+        const long long le = local_entry(ctx, entry[t]);
         if (le < 0) continue;
         ent.push_back(le);
         val.push_back(value[t]);
-        bits[node] |= (unsigned char)(1u << c);
     }
     cudaFree(ctx->cons_ent);
     cudaFree(ctx->cons_val);
@@ -998,22 +1035,9 @@ int petto_dev_set_constraints(petto_ctx* ctx, const int64_t* entry, const double
         CK(cudaMemcpyAsync(ctx->cons_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice,
                            ctx->stream));
     }
-    // mask bits 0-2 from the constraints; bit 3 (load) is preserved from set_source
-    std::vector<unsigned char> hmask;
-    hmask.resize((size_t)g.Ns);
-    CK(cudaMemcpyAsync(hmask.data(), ctx->mask, (size_t)g.Ns, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    for (auto& b : hmask) b &= 8u;
-    for (const auto& kv : bits) hmask[kv.first] |= kv.second;
-    CK(cudaMemcpyAsync(ctx->mask, hmask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
-    // pinned values into aux
-    if (ctx->ncons)
-        k_scatter_values<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->cons_val, ctx->ncons,
-                                                                          ctx->aux);
-    ctx->launches++;
-    CKL();
-    CK(cudaStreamSynchronize(ctx->stream));
-    return PETTO_OK;
+    ctx->cons_host = std::move(ent);
+    ctx->cons_vhost = std::move(val);
+    return rebuild_aux_mask(ctx);
 }
 
 int petto_dev_set_source(petto_ctx* ctx, const double* source) {
@@ -1031,50 +1055,19 @@ int petto_dev_set_source(petto_ctx* ctx, const double* source) {
         CK(cudaStreamSynchronize(ctx->stream));
         return PETTO_OK;
     }
-    // elasticity: sparse loads -> aux at unpinned entries, mask bit 3
-    std::vector<unsigned char> hmask((size_t)g.Ns);
-    CK(cudaMemcpyAsync(hmask.data(), ctx->mask, (size_t)g.Ns, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    std::vector<long long> idx;
-    std::vector<double> val;
-    for (auto& b : hmask) b &= 7u;
+    // elasticity: the nonzero loads of the owned planes (sparse in every preset)
+    ctx->load_host.clear();
+    ctx->load_vhost.clear();
     for (int c = 0; c < ctx->comps; ++c)
         for (long long n = (long long)g.kb * g.nx * g.ny; n < (long long)g.ke * g.nx * g.ny; ++n) {
             const double v = source[c * N + n];
             if (v == 0.0) continue;
-            long long node = 0;
-            int cc = 0;
-            const long long le = local_entry(ctx, c * N + n, &cc, &node);
+            const long long le = local_entry(ctx, c * N + n);
             if (le < 0) continue;
-            if (!((hmask[node] >> c) & 1)) {
-                idx.push_back(le);
-                val.push_back(v);
-            }
-            hmask[node] |= 8u;
+            ctx->load_host.push_back(le);
+            ctx->load_vhost.push_back(v);
         }
-    // clear stale loads (keep pinned values), then scatter
-    std::vector<long long> pins;
-    // aux := 0 except pinned entries
-    CK(cudaMemsetAsync(ctx->aux, 0, sizeof(double) * (size_t)g.Ns * ctx->comps, ctx->stream));
-    if (ctx->ncons)
-        k_scatter_values<<<blocks_for(ctx->ncons), 256, 0, ctx->stream>>>(ctx->cons_ent, ctx->cons_val, ctx->ncons,
-                                                                          ctx->aux);
-    if (!idx.empty()) {
-        long long* di = nullptr;
-        double* dv = nullptr;
-        CK(cudaMalloc(&di, sizeof(long long) * idx.size()));
-        CK(cudaMalloc(&dv, sizeof(double) * val.size()));
-        CK(cudaMemcpyAsync(di, idx.data(), sizeof(long long) * idx.size(), cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(dv, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice, ctx->stream));
-        k_scatter_values<<<blocks_for((long long)idx.size()), 256, 0, ctx->stream>>>(di, dv, (long long)idx.size(),
-                                                                                     ctx->aux);
-        CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(di);
-        cudaFree(dv);
-    }
-    CK(cudaMemcpyAsync(ctx->mask, hmask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    return PETTO_OK;
+    return rebuild_aux_mask(ctx);
 }
 
 int petto_dev_set_property(petto_ctx* ctx, const double* property) {

@@ -87,6 +87,37 @@ int main() {
         dev_op.residual(h1.current, r2);
         expect(r1.data == r2.data, "DeviceOperator::residual bit-identical to ElasticityOperator::residual");
     }
+    // 2b. the operators alias the caller's Lame fields, as run() relies on
+    // (optimizer.hpp:187-190): update_lame in place between two solves
+    {
+        const Grid g = Grid::make3d(20, 9, 8, 2.0, 1.0, 0.8);
+        BoundarySpec bc;
+        for (int f = 0; f < 6; ++f) bc.face[f] = {CondKind::TractionFree, 0.0, 0};
+        bc.face[XHi] = {CondKind::Dirichlet, 0.0, 0};
+        Field<double> E(g, 1);
+        for (Index i = 0; i < g.num_nodes(); ++i) E.data[i] = 0.2 + 0.8 * std::fmod(0.37 * i, 1.0);
+        ElasticMaterialField<double> lame_ref = make_lame(E, 0.3), lame_dev = make_lame(E, 0.3);
+        Field<double> loads(g, 3, 0.0);
+        loads.at(2, g.node(0, 4, 4)) = -1.0;
+        PTParams p;
+        p.dt_pt = g.min_spacing() * g.min_spacing() / 8;
+        p.dt_apt = 0.1 * g.min_spacing();
+        p.n_apt = 20;
+        p.n_pt = 5;
+        p.form = AptForm::SemiImplicitDamping;
+        const ElasticityOperator<double> ref_op(g, lame_ref, loads, bc);
+        const dev::ElasticityOperator dev_op(g, lame_dev, loads, bc, PETTO_MODE_REPLICA);
+        StateHistory<double> h1(Field<double>(g, 3, 0.0)), h2(Field<double>(g, 3, 0.0));
+        for (int loop = 0; loop < 3; ++loop) {
+            for (Index i = 0; i < g.num_nodes(); ++i) E.data[i] = 0.1 + 0.9 * std::fmod(0.53 * i + 0.17 * loop, 1.0);
+            update_lame(E, 0.3, lame_ref);
+            update_lame(E, 0.3, lame_dev);
+            hybrid_solve(h1, ref_op, p);
+            dev::hybrid_solve(h2, dev_op, p);
+        }
+        expect(h1.current.data == h2.current.data && h1.previous.data == h2.previous.data,
+               "dev::hybrid_solve sees in-place update_lame between solves (aliased material, replica)");
+    }
     // 3. iterate_to_tolerance on the criterion-1 Poisson box (n = 32)
     {
         const Grid g = Grid::make2d(32, 32, 1.0, 1.0);

@@ -421,3 +421,43 @@ def test_elastic2d_temporal_blocking_tile_edges(port, nx, ny):
     assert rel_err(a.current, b.current) < 1e-13 and rel_err(a.previous, b.previous) < 1e-13
     rc, wc, wp, _ = port.hybrid_solve(1, g, bc, E, 0.3, f, u0, u0, p)
     assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
+
+
+@pytest.mark.parametrize("mode", [FAST, REPLICA])
+@pytest.mark.parametrize("gi", [1, 4])
+def test_boundary_uploads_independent_of_order(port, gi, mode):
+    """set_constraints / set_source in either order, and a second set_constraints
+    with a different constraint set after the loads, give the same operator: the
+    context rebuilds its pinned values and loads from its own copies of both."""
+    g = ELASTIC_GRIDS[gi]
+    d = g.dim
+    E = H.random_modulus(g, 3)
+    u = H.random_field(d * g.num_nodes, 21)
+    f = H.sparse_loads(g, d, 5, count=40)
+    bc_a = H.elastic_bc(g, "x_lo")
+    bc_b = H.elastic_bc(g, "x_hi", pins=[(g.node(0, 0), 1, 0.25)])
+    ea, va = P.make_constraints(g, bc_a, d)
+    eb, vb = P.make_constraints(g, bc_b, d)
+    want = port.elasticity_residual(g, bc_b, E, 0.3, f, u)
+    outs = []
+    for order in ("cons_first", "loads_first", "replaced"):
+        ctx = D.Context(g, 1, 0.3, mode)
+        if order == "cons_first":
+            ctx.set_constraints(eb, vb)
+            ctx.set_source(f)
+        elif order == "loads_first":
+            ctx.set_source(f)
+            ctx.set_constraints(eb, vb)
+        else:  # an earlier constraint set, the loads, then the real constraint set
+            ctx.set_constraints(ea, va)
+            ctx.set_source(f)
+            ctx.set_constraints(eb, vb)
+        ctx.set_property(E)
+        ctx.init_operator()
+        ctx.set_state(u, u)
+        outs.append(ctx.residual()[0])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    if mode == REPLICA:
+        assert np.array_equal(outs[0], want)
+    else:
+        assert rel_err(outs[0], want) < 1e-12
