@@ -50,6 +50,9 @@ def args_():
                    help="slab ghost planes: stored by the fused kernel into the neighbours (peer) or NCCL send/recv")
     a.add_argument("--e2e-pipeline", type=int, default=3,
                    help="contexts driven from host threads in the e2e leg (copies overlap solves)")
+    a.add_argument("--layout", choices=["auto", "reference", "x"], default="auto",
+                   help="device layout: x-outermost (slabs along x, the longest axis) or the reference's; "
+                        "auto = x for 3D elasticity")
     a.add_argument("--no-cpu", action="store_true")
     a.add_argument("--cpu-steps", type=int, default=2, help="APT steps in the CPU baseline sample")
     return a.parse_args()
@@ -113,7 +116,7 @@ def config_dict(a, cfg, prob, sched, world):
                         f"form={'semi_implicit' if sched.pt.form else 'explicit'}",
             "l2": ("inputs larger than L2 (state 2x805 MB + modulus 268 MB per step)" if g.num_nodes > 8 << 20
                    else "working set L2-resident (grid smaller than L2); no flush"),
-            "parallelism": "1 GPU" if world == 1 else f"slab{world}: grid split along its outermost axis"}
+            "parallelism": "1 GPU" if world == 1 else f"slab{world}: grid split along its longest axis"}
 
 
 class ClockSampler:
@@ -272,9 +275,13 @@ def run_ours(a):
     N = g.num_nodes
     comps = prob.comps
     # strong scaling: the C5 grid is slab-decomposed along its outermost axis
-    k_range = slab.slab_range(rank, world, g.n[2]) if world > 1 else None
-    N_local = N if k_range is None else N // g.n[2] * (k_range[1] - k_range[0])
-    ctx = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local, k_range=k_range)
+    # strong scaling: the grid is slab-decomposed along its outermost device axis --
+    # x (the longest axis of the cantilever configs) in the x-outermost layout
+    xo = a.layout == "x" or (a.layout == "auto" and g.dim == 3 and prob.physics == 1)
+    axis = 0 if xo else 2
+    k_range = slab.slab_range(rank, world, g.n[axis]) if world > 1 else None
+    N_local = N if k_range is None else N // g.n[axis] * (k_range[1] - k_range[0])
+    ctx = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local, k_range=k_range, x_outermost=xo)
     ctx.set_constraints(prob.cons_entry, prob.cons_value)
     ctx.set_source(prob.source)
     ctx.set_property(E)
@@ -361,7 +368,8 @@ def run_ours(a):
         pipe = max(1, a.e2e_pipeline) if world == 1 else 1
         ctxs = [ctx]
         for _ in range(pipe - 1):
-            c2 = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local, k_range=k_range)
+            c2 = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local, k_range=k_range,
+                           x_outermost=xo)
             c2.set_constraints(prob.cons_entry, prob.cons_value)
             c2.set_source(prob.source)
             c2.set_property(E)
@@ -409,8 +417,8 @@ def run_ours(a):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
         # bytes copied by the whole job per step (each rank moves its planes + ghosts)
-        planes = [slab.stored_range(r, world, g.n[2]) for r in range(world)] if world > 1 else [(0, g.n[2])]
-        moved = sum(b - a0 for a0, b in planes) * (N // g.n[2]) * comps * 8
+        planes = [slab.stored_range(r, world, g.n[axis]) for r in range(world)] if world > 1 else [(0, g.n[axis])]
+        moved = sum(b - a0 for a0, b in planes) * (N // g.n[axis]) * comps * 8
         e2e = {"value": N * a.n_apt * e2e_steps / dt / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 2 * moved, "d2h_bytes_per_step": 2 * comps * N * 8,
                "steps": e2e_steps, "pipeline": f"{pipe} contexts from {pipe} host threads"
@@ -440,6 +448,7 @@ def run_ours(a):
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (reference {a.config} problem: initial design, zero state)",
         "config": config_dict(a, cfg, prob, sched, world),
+        "layout": "x-outermost (device axes y, z, x; uploads/downloads permute)" if xo else "reference (x fastest)",
         "halo": None if world == 1 else ("peer stores from the fused kernel (CUDA IPC, NVLink)" if a.halo == "peer"
                                          else "NCCL send/recv every step"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -63,6 +63,12 @@ typedef struct {
     /* slab decomposition along the outermost axis (k): this rank owns node
      * planes [k_begin, k_end) of the global grid.  Single GPU: 0, n[2]. */
     int64_t k_begin, k_end;
+    /* 3D, FAST mode: keep the grid in HBM with x as the outermost (slab) axis --
+     * device axes (y, z, x), displacement components permuted alike; uploads and
+     * downloads permute, the host side keeps the reference's x-fastest layout
+     * (grid.hpp:47).  Then k_begin/k_end are x planes: slabs along the longest
+     * axis of an x-elongated grid.  0: the reference layout. */
+    int x_outermost;
 } petto_grid_desc;
 
 /* PTParams (state_solver.hpp:17-34); form 0 ExplicitDamping, 1 SemiImplicitDamping. */

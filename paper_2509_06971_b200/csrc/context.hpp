@@ -30,6 +30,14 @@ struct PeerSlab {
 struct petto_ctx {
     petto_grid_desc desc{};
     petto_b200::Geo g{};
+    // x-outermost layout (petto_grid_desc.x_outermost): device axes (y, z, x) of the
+    // host grid; host (i, j, k) -> device (j, k, i), host component c -> (c + 2) % 3
+    bool perm = false;
+    double* stage[2] = {nullptr, nullptr};  // permuting uploads / downloads: host-order components,
+    size_t stage_elems = 0;                 // two buffers so one transfer's copy overlaps the
+    int stage_next = 0;                     // previous one's permutation
+    cudaStream_t xstream = nullptr;  // high-priority stream of the permutation kernels
+    cudaEvent_t xev[2] = {nullptr, nullptr};
     int comps = 1;
     int mode = PETTO_MODE_FAST;
     int device = 0;

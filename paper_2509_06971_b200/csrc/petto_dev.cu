@@ -64,10 +64,132 @@ long long owned_nodes(const petto_ctx* ctx) {
 
 int blocks_for(long long n, int threads = 256) { return (int)std::max(1LL, (n + threads - 1) / threads); }
 
-// Host (global, dense) <-> device (local, pitched) copies of `comps` components.
-int upload(petto_ctx* ctx, double* dst, const double* host, int comps) {
+// ------------------------------------------------- x-outermost permutation
+// Host layout x-fastest (grid.hpp:47); device layout of a permuted context: axes
+// (y, z, x).  A rank's stored x planes [ks0, ks0 + nzs) of `comps` host components
+// sit in the staging buffer as [c][z][y][x - ks0]; these kernels move them to /
+// from the pitched device layout with 32 x 32 shared-memory tiles (coalesced on
+// both sides).  Host extents: nxh = stored (or owned) x planes, ny = g.nx, nz =
+// g.ny.  cperm: device component of host component c is (c + 2) % 3.
+__global__ void k_perm_in(Geo g, const double* __restrict__ stage, int nxh, int comps, bool cperm,
+                          double* __restrict__ dst) {
+    __shared__ double tile[32][33];
+    const int z = blockIdx.z;                       // host z = device j
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int c = 0; c < comps; ++c) {
+        const double* sc = stage + (long long)c * g.nx * g.ny * nxh;
+        double* dc = dst + (long long)(cperm ? (c + 2) % 3 : c) * g.Ns;
+        for (int r = ty; r < 32; r += 8) {
+            const int y = y0 + r, x = x0 + tx;      // read along host x
+            if (y < g.nx && x < nxh) tile[r][tx] = sc[((long long)z * g.nx + y) * nxh + x];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int x = x0 + r, y = y0 + tx;      // write along device x (= host y)
+            if (y < g.nx && x < nxh) dc[((long long)x * g.ny + z) * g.px + y] = tile[tx][r];
+        }
+        __syncthreads();
+    }
+}
+
+// device planes [k0, k0 + nxh) -> staging [c][z][y][x - k0]
+__global__ void k_perm_out(Geo g, const double* __restrict__ src, int k0, int nxh, int comps, bool cperm,
+                           double* __restrict__ stage) {
+    __shared__ double tile[32][33];
+    const int z = blockIdx.z;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int c = 0; c < comps; ++c) {
+        const double* sc = src + (long long)(cperm ? (c + 2) % 3 : c) * g.Ns;
+        double* dc = stage + (long long)c * g.nx * g.ny * nxh;
+        for (int r = ty; r < 32; r += 8) {
+            const int x = x0 + r, y = y0 + tx;      // read along device x (= host y)
+            if (y < g.nx && x < nxh) tile[r][tx] = sc[((long long)(k0 - g.ks0 + x) * g.ny + z) * g.px + y];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int y = y0 + r, x = x0 + tx;      // write along host x
+            if (y < g.nx && x < nxh) dc[((long long)z * g.nx + y) * nxh + x] = tile[tx][r];
+        }
+        __syncthreads();
+    }
+}
+
+// staging buffer for the next permuted transfer (alternating between two)
+double* stage_reserve(petto_ctx* ctx, size_t elems) {
+    if (!ctx->xstream) {
+        // the permutations run on a high-priority stream: when several contexts share
+        // the GPU (a pipelined caller), they slip in between another context's steps
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) hi = 0;
+        if (const char* e = std::getenv("PETTO_XPRIO")) hi = e[0] == '0' ? lo : hi;  // A/B of the priority
+        if (
+            cudaStreamCreateWithPriority(&ctx->xstream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->xev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->xev[1], cudaEventDisableTiming) != cudaSuccess) {
+            fail(ctx, PETTO_ERROR, "permutation stream creation failed");
+            return nullptr;
+        }
+    }
+    if (ctx->stage_elems < elems) {
+        for (double*& b : ctx->stage) {
+            cudaFree(b);
+            b = nullptr;
+        }
+        ctx->stage_elems = 0;
+        for (double*& b : ctx->stage)
+            if (cudaMalloc(&b, sizeof(double) * elems) != cudaSuccess) {
+                fail(ctx, PETTO_ERROR, "out of device memory (staging)");
+                return nullptr;
+            }
+        ctx->stage_elems = elems;
+    }
+    double* b = ctx->stage[ctx->stage_next];
+    ctx->stage_next ^= 1;
+    return b;
+}
+
+// main stream -> permutation stream -> main stream
+int xfer_fork(petto_ctx* ctx) {
+    CK(cudaEventRecord(ctx->xev[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->xstream, ctx->xev[0], 0));
+    return PETTO_OK;
+}
+int xfer_join(petto_ctx* ctx) {
+    CK(cudaEventRecord(ctx->xev[1], ctx->xstream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->xev[1], 0));
+    return PETTO_OK;
+}
+
+// device component of host component c of a displacement-like field (3D elasticity)
+int dev_comp(const petto_ctx* ctx, int c, bool vec) { return ctx->perm && vec && ctx->comps == 3 ? (c + 2) % 3 : c; }
+
+// Host (global, dense) <-> device (local, pitched) copies of `comps` components;
+// vec: a displacement-like field whose components follow the axes.
+int upload(petto_ctx* ctx, double* dst, const double* host, int comps, bool vec = false) {
     const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
+    if (ctx->perm) {
+        // host x planes [ks0, ks0 + nzs) of every component into the staging buffer
+        // (rows of nzs doubles, host pitch nx_host = g.nz), then one permutation
+        const size_t elems = (size_t)g.nzs * g.nx * g.ny;
+        double* stage = stage_reserve(ctx, elems * comps);
+        if (!stage) return PETTO_ERROR;
+        if (g.nzs == g.nz)
+            CK(cudaMemcpyAsync(stage, host, sizeof(double) * elems * comps, cudaMemcpyHostToDevice, ctx->stream));
+        else
+            for (int c = 0; c < comps; ++c)
+                CK(cudaMemcpy2DAsync(stage + c * elems, (size_t)g.nzs * 8, host + c * N + g.ks0,
+                                     (size_t)g.nz * 8, (size_t)g.nzs * 8, (size_t)g.nx * g.ny, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        if (int rc = xfer_fork(ctx)) return rc;
+        const dim3 grid((g.nzs + 31) / 32, (g.nx + 31) / 32, g.ny), blk(32, 8);
+        k_perm_in<<<grid, blk, 0, ctx->xstream>>>(g, stage, g.nzs, comps, vec && ctx->comps == 3, dst);
+        ctx->launches++;
+        CKL();
+        return xfer_join(ctx);
+    }
     for (int c = 0; c < comps; ++c) {
         const double* src = host + c * N + (long long)g.ks0 * g.nx * g.ny;
         if (g.px == g.nx)  // unpadded rows: one linear copy (full copy-engine rate)
@@ -80,9 +202,28 @@ int upload(petto_ctx* ctx, double* dst, const double* host, int comps) {
     return PETTO_OK;
 }
 
-int download(petto_ctx* ctx, double* host, const double* src, int comps) {
+int download(petto_ctx* ctx, double* host, const double* src, int comps, bool vec = false) {
     const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
+    if (ctx->perm) {
+        const int nxo = g.ke - g.kb;
+        const size_t elems = (size_t)nxo * g.nx * g.ny;
+        double* stage = stage_reserve(ctx, elems * comps);
+        if (!stage) return PETTO_ERROR;
+        if (int rc = xfer_fork(ctx)) return rc;
+        const dim3 grid((nxo + 31) / 32, (g.nx + 31) / 32, g.ny), blk(32, 8);
+        k_perm_out<<<grid, blk, 0, ctx->xstream>>>(g, src, g.kb, nxo, comps, vec && ctx->comps == 3, stage);
+        ctx->launches++;
+        CKL();
+        if (int rc = xfer_join(ctx)) return rc;
+        if (nxo == g.nz)
+            CK(cudaMemcpyAsync(host, stage, sizeof(double) * elems * comps, cudaMemcpyDeviceToHost, ctx->stream));
+        else
+            for (int c = 0; c < comps; ++c)
+                CK(cudaMemcpy2DAsync(host + c * N + g.kb, (size_t)g.nz * 8, stage + c * elems, (size_t)nxo * 8,
+                                     (size_t)nxo * 8, (size_t)g.nx * g.ny, cudaMemcpyDeviceToHost, ctx->stream));
+        return PETTO_OK;
+    }
     for (int c = 0; c < comps; ++c) {
         double* dst = host + c * N + (long long)g.kb * g.nx * g.ny;
         const double* s = src + c * g.Ns + lidx(g, 0, 0, g.kb);
@@ -96,21 +237,39 @@ int download(petto_ctx* ctx, double* host, const double* src, int comps) {
     return PETTO_OK;
 }
 
+// Host global node -> device (i, j, k) of the device grid.
+void host_to_dev(const petto_ctx* ctx, long long node, int& i, int& j, int& k) {
+    const Geo& g = ctx->g;
+    if (ctx->perm) {  // host dims (nz, nx, ny) of the device grid
+        const long long plane = (long long)g.nz * g.nx;
+        const int hk = (int)(node / plane);
+        const long long r = node - (long long)hk * plane;
+        const int hj = (int)(r / g.nz), hi = (int)(r - (long long)hj * g.nz);
+        i = hj;
+        j = hk;
+        k = hi;
+        return;
+    }
+    const long long plane = (long long)g.nx * g.ny;
+    k = (int)(node / plane);
+    const long long r = node - (long long)k * plane;
+    j = (int)(r / g.nx);
+    i = (int)(r - (long long)j * g.nx);
+}
+
 // Global entry comp*N + node -> local entry comp*Ns + lidx, or -1 if the node is
 // not on an owned plane of this rank.
 long long local_entry(const petto_ctx* ctx, long long e, int* comp = nullptr, long long* node_out = nullptr) {
     const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
     const int c = (int)(e / N);
-    const long long node = e - (long long)c * N;
-    const long long plane = (long long)g.nx * g.ny;
-    const int k = (int)(node / plane);
-    const long long r = node - (long long)k * plane;
-    const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
+    int i, j, k;
+    host_to_dev(ctx, e - (long long)c * N, i, j, k);
     if (k < g.kb || k >= g.ke) return -1;
-    if (comp) *comp = c;
+    const int cd = dev_comp(ctx, c, true);
+    if (comp) *comp = cd;
     if (node_out) *node_out = lidx(g, i, j, k);
-    return c * g.Ns + lidx(g, i, j, k);
+    return cd * g.Ns + lidx(g, i, j, k);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -330,6 +489,7 @@ void plan_3d(const petto_ctx* ctx, int nstrips, int& chunk, int& nitems, int& gr
             chunk = L;
         }
     }
+    if (const char* e = std::getenv("PETTO_CHUNK")) chunk = std::max(2, std::min(e3::LMAX, std::atoi(e) & ~1));  // A/B
     nitems = nstrips * ((nzo + chunk - 1) / chunk);
     grid = std::min(ctx->nsm, nitems);
 }
@@ -721,6 +881,8 @@ int writer_source(petto_ctx* ctx, int field, int index, wr::Src* out) {
     const Geo& g = ctx->g;
     if (g.kb != 0 || g.ke != g.nz)
         return fail(ctx, PETTO_INVALID, "writers need the whole grid in one context (slab rank: gather first)");
+    if (ctx->perm)
+        return fail(ctx, PETTO_INVALID, "writers need the reference layout (x_outermost context: download first)");
     const double* base = nullptr;
     if (field == PETTO_FIELD_STATE) {
         if (index < 0 || index >= ctx->comps) return fail(ctx, PETTO_INVALID, "writer: state component out of range");
@@ -862,6 +1024,24 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     g.nz = d->dim == 3 ? (int)d->n[2] : 1;
     for (int a = 0; a < 3; ++a) g.h[a] = 1.0;
     for (int a = 0; a < d->dim; ++a) g.h[a] = d->length[a] / (double)(d->n[a] - 1);
+    if (d->x_outermost) {
+        // device axes (y, z, x): the unit-cell stiffness, lumped volumes and every
+        // kernel follow from the device spacings (an axis relabelling of an
+        // isotropic operator); the reference's operation order is not kept, so
+        // REPLICA mode is refused
+        if (d->dim != 3 || d->mode != PETTO_MODE_FAST) {
+            delete ctx;
+            return fail(nullptr, PETTO_INVALID, "x_outermost: 3D grids in FAST mode only");
+        }
+        ctx->perm = true;
+        const double h[3] = {g.h[0], g.h[1], g.h[2]};
+        g.nx = (int)d->n[1];
+        g.ny = (int)d->n[2];
+        g.nz = (int)d->n[0];
+        g.h[0] = h[1];
+        g.h[1] = h[2];
+        g.h[2] = h[0];
+    }
     g.kb = (int)(d->k_end > d->k_begin ? d->k_begin : 0);
     g.ke = (int)(d->k_end > d->k_begin ? d->k_end : g.nz);
     if (g.kb < 0 || g.ke > g.nz || g.kb >= g.ke) {
@@ -871,6 +1051,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     g.ks0 = std::max(0, g.kb - 1);
     g.nzs = std::min(g.nz, g.ke + 1) - g.ks0;
     g.px = (g.nx + 15) / 16 * 16;
+    if (const char* e = std::getenv("PETTO_PITCH_PAD")) g.px += (std::atoi(e) + 15) / 16 * 16;  // layout A/B
     g.Ns = (long long)g.px * g.ny * g.nzs;
 
     auto cleanup = [&](const std::string& m) {
@@ -928,6 +1109,10 @@ void petto_dev_destroy(petto_ctx* ctx) {
     if (ctx->ev_pull) cudaEventDestroy(ctx->ev_pull);
     if (ctx->ev_team) cudaEventDestroy(ctx->ev_team);
     cudaFree(ctx->team_buf);
+    for (double* b : ctx->stage) cudaFree(b);
+    if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
+    for (cudaEvent_t e : ctx->xev)
+        if (e) cudaEventDestroy(e);
     for (int b = 0; b < 3; ++b) cudaFree(ctx->st[b]);
     cudaFree(ctx->prop);
     cudaFree(ctx->ecell);
@@ -964,6 +1149,7 @@ void petto_dev_destroy(petto_ctx* ctx) {
 
 int petto_dev_set_mode(petto_ctx* ctx, int mode) {
     if (mode != PETTO_MODE_FAST && mode != PETTO_MODE_REPLICA) return fail(ctx, PETTO_INVALID, "unknown mode");
+    if (ctx->perm && mode != PETTO_MODE_FAST) return fail(ctx, PETTO_INVALID, "x_outermost: FAST mode only");
     ctx->mode = mode;
     return PETTO_OK;
 }
@@ -1042,31 +1228,28 @@ int petto_dev_set_constraints(petto_ctx* ctx, const int64_t* entry, const double
 
 int petto_dev_set_source(petto_ctx* ctx, const double* source) {
     CK(cudaSetDevice(ctx->device));
-    const Geo& g = ctx->g;
     const long long N = global_nodes(ctx);
-    if (int rc = upload(ctx, ctx->src, source, ctx->comps)) return rc;
+    if (int rc = upload(ctx, ctx->src, source, ctx->comps, true)) return rc;
     if (ctx->desc.physics == 0) {
         // uniform source: the fused kernel reads a scalar instead of a field
         bool uni = true;
-        for (long long n = (long long)g.kb * g.nx * g.ny; n < (long long)g.ke * g.nx * g.ny && uni; ++n)
-            uni = source[n] == source[(long long)g.kb * g.nx * g.ny];
+        for (long long n = 1; n < N && uni; ++n) uni = source[n] == source[0];
         ctx->src_uniform = uni;
-        ctx->src_value = source[(long long)g.kb * g.nx * g.ny];
+        ctx->src_value = source[0];
         CK(cudaStreamSynchronize(ctx->stream));
         return PETTO_OK;
     }
     // elasticity: the nonzero loads of the owned planes (sparse in every preset)
     ctx->load_host.clear();
     ctx->load_vhost.clear();
-    for (int c = 0; c < ctx->comps; ++c)
-        for (long long n = (long long)g.kb * g.nx * g.ny; n < (long long)g.ke * g.nx * g.ny; ++n) {
-            const double v = source[c * N + n];
-            if (v == 0.0) continue;
-            const long long le = local_entry(ctx, c * N + n);
-            if (le < 0) continue;
-            ctx->load_host.push_back(le);
-            ctx->load_vhost.push_back(v);
-        }
+    for (long long e = 0; e < ctx->comps * N; ++e) {
+        const double v = source[e];
+        if (v == 0.0) continue;
+        const long long le = local_entry(ctx, e);
+        if (le < 0) continue;
+        ctx->load_host.push_back(le);
+        ctx->load_vhost.push_back(v);
+    }
     return rebuild_aux_mask(ctx);
 }
 
@@ -1160,8 +1343,8 @@ int petto_dev_set_state(petto_ctx* ctx, const double* current, const double* pre
     const unsigned long long seq = ctx->peer_halo ? ++ctx->peer_seq : 0;
     if (seq)
         if (int rc = peer_wait(ctx, seq)) return rc;
-    if (int rc = upload(ctx, ctx->st[0], current, ctx->comps)) return rc;
-    if (int rc = upload(ctx, ctx->st[1], previous ? previous : current, ctx->comps)) return rc;
+    if (int rc = upload(ctx, ctx->st[0], current, ctx->comps, true)) return rc;
+    if (int rc = upload(ctx, ctx->st[1], previous ? previous : current, ctx->comps, true)) return rc;
     if (seq)
         if (int rc = peer_signal(ctx, seq)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1172,9 +1355,9 @@ int petto_dev_set_state(petto_ctx* ctx, const double* current, const double* pre
 int petto_dev_get_state(petto_ctx* ctx, double* current, double* previous) {
     CK(cudaSetDevice(ctx->device));
     if (current)
-        if (int rc = download(ctx, current, ctx->st[ctx->cur], ctx->comps)) return rc;
+        if (int rc = download(ctx, current, ctx->st[ctx->cur], ctx->comps, true)) return rc;
     if (previous)
-        if (int rc = download(ctx, previous, ctx->st[ctx->prev], ctx->comps)) return rc;
+        if (int rc = download(ctx, previous, ctx->st[ctx->prev], ctx->comps, true)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
     return PETTO_OK;
 }
@@ -1431,25 +1614,20 @@ int petto_dev_set_design(petto_ctx* ctx, const petto_material* m, const petto_ta
     CK(cudaMemsetAsync(ctx->gc, 0, sizeof(double) * P * g.Ns, ctx->stream));
     CK(cudaMemsetAsync(ctx->scratch1, 0, sizeof(double) * g.Ns, ctx->stream));
     CK(cudaMemsetAsync(ctx->dscal, 0, sizeof(double) * 256, ctx->stream));
+    // region: per stored node mask, and the owned region nodes in list order as
+    // device-grid node ids (k_region_terms decodes them with the device dims)
     std::vector<unsigned char> mask((size_t)g.Ns, 0);
-    const long long plane = (long long)g.nx * g.ny;
+    std::vector<long long> own;
     for (int64_t node : ctx->region_nodes) {
         if (node < 0 || node >= global_nodes(ctx)) return fail(ctx, PETTO_INVALID, "region node outside the grid");
-        const int k = (int)(node / plane);
-        if (k < g.ks0 || k >= g.ks0 + g.nzs) continue;
-        const long long r = node - (long long)k * plane;
-        const int j = (int)(r / g.nx), i = (int)(r - (long long)j * g.nx);
-        mask[lidx(g, i, j, k)] = 1;
+        int i, j, k;
+        host_to_dev(ctx, node, i, j, k);
+        if (k >= g.ks0 && k < g.ks0 + g.nzs) mask[lidx(g, i, j, k)] = 1;
+        if (k >= g.kb && k < g.ke) own.push_back(((long long)k * g.ny + j) * g.nx + i);
     }
     CK(cudaMalloc(&ctx->region_mask, (size_t)g.Ns));
     CK(cudaMemcpyAsync(ctx->region_mask, mask.data(), (size_t)g.Ns, cudaMemcpyHostToDevice, ctx->stream));
     if (!ctx->region_nodes.empty()) {
-        // region sums run over this rank's owned planes only (list order kept)
-        std::vector<long long> own;
-        for (int64_t node : ctx->region_nodes) {
-            const int k = (int)(node / plane);
-            if (k >= g.kb && k < g.ke) own.push_back(node);
-        }
         ctx->region_nodes.assign(own.begin(), own.end());
         CK(cudaMalloc(&ctx->region_dev, sizeof(long long) * std::max<size_t>(own.size(), 1)));
         if (!own.empty())
@@ -1508,10 +1686,12 @@ using DblOf = std::function<double*(petto_ctx*)>;
 bool is_slab(const petto_ctx* ctx) { return ctx->g.kb != 0 || ctx->g.ke != ctx->g.nz; }
 
 // A context used on its own: a slab needs its communicator for the collectives.
+// (A lone slab may still run the state solve: its ghost planes then stay as
+// uploaded, or follow the peer halo -- used for timing one rank's share.)
 int solo_ok(petto_ctx* ctx, bool solve_only) {
     if (ctx->nb_lo || ctx->nb_hi)
         return fail(ctx, PETTO_INVALID, "slab context is linked in a local group: use the petto_dev_group_* calls");
-    if (is_slab(ctx) && !ctx->nccl_comm && !(solve_only && ctx->peer_halo))
+    if (is_slab(ctx) && !ctx->nccl_comm && !solve_only)
         return fail(ctx, PETTO_INVALID, "slab context without a communicator (petto_dev_comm_init)");
     return PETTO_OK;
 }
@@ -2201,7 +2381,7 @@ int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {
     if (int rc = solo_ok(ctx, false)) return rc;
     if (int rc = team_residual(Team{&ctx, 1}, r_pde)) return rc;
     if (out) {
-        if (int rc = download(ctx, out, ctx->r, ctx->comps)) return rc;
+        if (int rc = download(ctx, out, ctx->r, ctx->comps, true)) return rc;
         CK(cudaStreamSynchronize(ctx->stream));
     }
     return PETTO_OK;

@@ -45,7 +45,7 @@ class GridDesc(C.Structure):
     _fields_ = [
         ("dim", C.c_int), ("n", C.c_int64 * 3), ("length", C.c_double * 3), ("physics", C.c_int),
         ("poisson_ratio", C.c_double), ("mode", C.c_int), ("device", C.c_int),
-        ("k_begin", C.c_int64), ("k_end", C.c_int64),
+        ("k_begin", C.c_int64), ("k_end", C.c_int64), ("x_outermost", C.c_int),
     ]
 
 
@@ -247,7 +247,10 @@ def pt_params(p):
 class Context:
     """One problem resident in HBM (a petto_ctx)."""
 
-    def __init__(self, grid, physics, poisson_ratio=0.3, mode=MODE_FAST, device=0, k_range=None):
+    def __init__(self, grid, physics, poisson_ratio=0.3, mode=MODE_FAST, device=0, k_range=None,
+                 x_outermost=False):
+        """k_range: this slab's planes of the outermost device axis -- z, or x with
+        x_outermost (the device keeps (y, z, x); uploads / downloads permute)."""
         L = lib()
         self.grid = grid
         self.physics = physics
@@ -255,7 +258,7 @@ class Context:
         self.N = grid.num_nodes
         kb, ke = k_range if k_range else (0, 0)
         d = GridDesc(grid.dim, (C.c_int64 * 3)(*grid.n), (C.c_double * 3)(*grid.length), physics, poisson_ratio,
-                     mode, device, kb, ke)
+                     mode, device, kb, ke, 1 if x_outermost else 0)
         h = C.c_void_p()
         rc = L.petto_dev_create(C.byref(d), C.byref(h))
         if rc != OK:
@@ -412,9 +415,9 @@ class Context:
         return res, records
 
     @staticmethod
-    def from_problem(prob, mode=MODE_FAST, device=0, k_range=None):
+    def from_problem(prob, mode=MODE_FAST, device=0, k_range=None, x_outermost=False):
         """Upload a problem.Problem (build_problem's product) as run() expects it."""
-        ctx = Context(prob.grid, prob.physics, prob.poisson_ratio, mode, device, k_range)
+        ctx = Context(prob.grid, prob.physics, prob.poisson_ratio, mode, device, k_range, x_outermost)
         ctx.set_constraints(prob.cons_entry, prob.cons_value)
         ctx.set_source(prob.source)
         ctx.set_design(prob.physics, prob.properties, prob.poisson_ratio, prob.penalty, prob.void_floor,
