@@ -440,7 +440,9 @@ def run_ours(a):
         with open(prof) as f:
             d = json.load(f)
         cap = d.get(kname, {})
-        if cap.get("config", "C5") == a.config and world == 1:  # the capture's own workload only
+        layout = "x-outermost" if xo else "reference"
+        if cap.get("config", "C5") == a.config and world == 1 and cap.get("layout", "reference") == layout:
+            # the capture's own workload and layout only
             traffic = cap.get("dram_bytes_per_launch")
 
     line = {
