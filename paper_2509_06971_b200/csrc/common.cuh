@@ -19,7 +19,19 @@ struct Geo {
     int px;          // row pitch (elements)
     long long Ns;    // stored nodes incl. padding = px * ny * nzs
     double h[3];
+    double hih[3];   // 0.5 / h  (stencil.hpp:23-31 derivative factor; host IEEE division = the device's)
+    double ilap[3];  // 1 / (h h) (stencil.hpp:109-116 Laplacian factor)
 };
+
+// The per-axis stencil factors the design kernels need at every node, computed
+// once (same IEEE operations as the reference's per-call expressions).
+inline void geo_factors(Geo& g) {
+    for (int a = 0; a < 3; ++a) {
+        g.hih[a] = 0.5 / g.h[a];
+        const double h2 = g.h[a] * g.h[a];
+        g.ilap[a] = 1.0 / h2;
+    }
+}
 
 // Device-resident control block of a context: non-finite detection with the
 // reference's check_finite cadence (state_solver.hpp:463-497) and the

@@ -64,6 +64,14 @@ long long owned_nodes(const petto_ctx* ctx) {
 
 int blocks_for(long long n, int threads = 256) { return (int)std::max(1LL, (n + threads - 1) / threads); }
 
+// launch shape of the z-streamed 3D sensitivity kernel
+constexpr int SENS_ZC = 16;
+dim3 sens_grid(const petto_ctx* x) {
+    const Geo& g = x->g;
+    return dim3((g.nx + 31) / 32, (g.ny + 3) / 4, (g.ke - g.kb + SENS_ZC - 1) / SENS_ZC);
+}
+
+
 // ------------------------------------------------- x-outermost permutation
 // Host layout x-fastest (grid.hpp:47); device layout of a permuted context: axes
 // (y, z, x).  A rank's stored x planes [ks0, ks0 + nzs) of `comps` host components
@@ -1048,6 +1056,7 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         delete ctx;
         return fail(nullptr, PETTO_INVALID, "slab: need 0 <= k_begin < k_end <= nz");
     }
+    geo_factors(g);
     g.ks0 = std::max(0, g.kb - 1);
     g.nzs = std::min(g.nz, g.ke + 1) - g.ks0;
     g.px = (g.nx + 15) / 16 * 16;
@@ -1073,7 +1082,9 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     cudaMemsetAsync(ctx->mask, 0, (size_t)g.Ns, ctx->stream);
     cudaMemsetAsync(ctx->src, 0, fb * ctx->comps, ctx->stream);
     cudaMemsetAsync(ctx->r, 0, fb * ctx->comps, ctx->stream);
-    ctx->npartials = std::max(4 * ctx->nsm, 1024);
+    // block partials of the reductions: enough blocks (32 per SM) for the design
+    // loop's grid-stride passes to keep HBM busy, one partial each
+    ctx->npartials = std::max(32 * ctx->nsm, 1024);
     if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D solves
     if (const char* e = std::getenv("PETTO_NO_PDL")) ctx->no_pdl = e[0] == '1';        // A/B of the 3D step overlap
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
@@ -1608,7 +1619,10 @@ int petto_dev_set_design(petto_ctx* ctx, const petto_material* m, const petto_ta
     CK(cudaMalloc(&ctx->scratch1, sizeof(double) * g.Ns));
     CK(cudaMalloc(&ctx->term1, sizeof(double) * std::max<long long>(owned, (long long)ctx->region_nodes.size() + 1)));
     CK(cudaMalloc(&ctx->term2, sizeof(double) * owned));
-    CK(cudaMalloc(&ctx->pmax, sizeof(double) * 8 * ctx->npartials));
+    {
+        const dim3 sg = sens_grid(ctx);  // block maxima of the sensitivity kernels, partials of the FAST sums
+        CK(cudaMalloc(&ctx->pmax, sizeof(double) * 8 * std::max<long long>(ctx->npartials, (long long)sg.x * sg.y * sg.z)));
+    }
     CK(cudaMalloc(&ctx->count, sizeof(unsigned long long)));
     CK(cudaMemsetAsync(ctx->phases, 0, sizeof(double) * P * g.Ns, ctx->stream));
     CK(cudaMemsetAsync(ctx->gc, 0, sizeof(double) * P * g.Ns, ctx->stream));
@@ -1847,6 +1861,23 @@ int team_sum_terms(Team t, const DblOf& term, const std::function<long long(pett
     return team_reduce(t, [&](petto_ctx* x) -> void* { return dst(x); }, 1, RED_SUM);
 }
 
+// FAST: the sum of block partials a kernel left in partials(ctx)[0, nparts(ctx)),
+// into dst(ctx) of every context (same tree as team_sum_terms' FAST branch).
+int team_sum_partials(Team t, const DblOf& partials, const std::function<int(petto_ctx*)>& nparts,
+                      const DblOf& dst) {
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        k_sum_finish<<<1, 256, 0, ctx->stream>>>(partials(ctx), nparts(ctx), dst(ctx));
+        ctx->launches++;
+        CKL();
+    }
+    return team_reduce(t, [&](petto_ctx* x) -> void* { return dst(x); }, 1, RED_SUM);
+}
+
+// grid of the FAST partial-sum kernels: the partition k_sum_partials uses
+int sum_grid(const petto_ctx* ctx) { return (int)std::min<long long>(ctx->npartials, blocks_for(owned_nodes(ctx))); }
+
 // Ghost planes of `comps` fields starting at f(ctx) (component stride Ns).
 int team_halo(Team t, const DblOf& f, int comps) {
     if (t.n == 1) return t.nccl() ? halo_ptr(t.lead(), f(t.lead()), comps) : PETTO_OK;
@@ -2009,6 +2040,20 @@ long long owned_of(petto_ctx* x) { return owned_nodes(x); }
 // phase_mass per phase (phase_field.hpp:83-102) into dscal[slot + q]
 int team_phase_masses(Team t, int slot) {
     for (int q = 0; q < t.lead()->mat.nphases; ++q) {
+        if (!t.replica()) {  // block partials straight from phi (no term array)
+            for (int i = 0; i < t.n; ++i) {
+                petto_ctx* ctx = t.c[i];
+                CK(cudaSetDevice(ctx->device));
+                k_mass_partials<<<sum_grid(ctx), 256, 0, ctx->stream>>>(ctx->g, ctx->phases + q * ctx->g.Ns,
+                                                                        ctx->pmax);
+                ctx->launches++;
+                CKL();
+            }
+            if (int rc = team_sum_partials(t, [](petto_ctx* x) { return x->pmax; }, sum_grid,
+                                           [&](petto_ctx* x) { return x->dscal + slot + q; }))
+                return rc;
+            continue;
+        }
         for (int i = 0; i < t.n; ++i) {
             petto_ctx* ctx = t.c[i];
             CK(cudaSetDevice(ctx->device));
@@ -2106,10 +2151,33 @@ int team_design_update(Team t) {
     for (int i = 0; i < t.n; ++i) {
         petto_ctx* x = t.c[i];
         CK(cudaSetDevice(x->device));
-        const int nb = (int)std::min<long long>(x->npartials, blocks_for(owned_nodes(x)));
-        k_sens_gc<<<nb, 256, 0, x->stream>>>(x->g, d, x->mat.kind, ctr, cec, x->phases, x->st[x->cur], x->gc,
-                                             x->pmax);
-        k_local_gmax<<<1, 32, 0, x->stream>>>(d.np, x->pmax, nb, x->dscal);
+        int nb = (int)std::min<long long>(x->npartials, blocks_for(owned_nodes(x)));
+        if (x->g.dim == 3 && d.np <= 4) {
+            // z-streamed (every node of u read once), one block per 32 x 4 columns x SENS_ZC planes
+            const dim3 grid3 = sens_grid(x), blk(32, 4);
+            nb = (int)(grid3.x * grid3.y * grid3.z);
+            auto launch = [&](auto np_c, auto kind_c) {
+                k_sens_gc3<decltype(np_c)::value, decltype(kind_c)::value><<<grid3, blk, 0, x->stream>>>(
+                    x->g, d, ctr, cec, x->phases, x->st[x->cur], x->gc, x->pmax, SENS_ZC);
+            };
+            auto by_kind = [&](auto np_c) {
+                if (x->mat.kind == 0) launch(np_c, std::integral_constant<int, 0>{});
+                else launch(np_c, std::integral_constant<int, 1>{});
+            };
+            switch (d.np) {
+                case 1: by_kind(std::integral_constant<int, 1>{}); break;
+                case 2: by_kind(std::integral_constant<int, 2>{}); break;
+                case 3: by_kind(std::integral_constant<int, 3>{}); break;
+                default: by_kind(std::integral_constant<int, 4>{}); break;
+            }
+        } else if (x->g.dim == 3) {
+            k_sens_gc<3><<<nb, 256, 0, x->stream>>>(x->g, d, x->mat.kind, ctr, cec, x->phases, x->st[x->cur], x->gc,
+                                                    x->pmax);
+        } else {
+            k_sens_gc<2><<<nb, 256, 0, x->stream>>>(x->g, d, x->mat.kind, ctr, cec, x->phases, x->st[x->cur], x->gc,
+                                                    x->pmax);
+        }
+        k_local_gmax<<<1, 32 * d.np, 0, x->stream>>>(d.np, x->pmax, nb, x->dscal);
         x->launches += 2;
         if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "sensitivity launch failed");
     }
@@ -2132,8 +2200,15 @@ int team_design_update(Team t) {
         petto_ctx* x = t.c[i];
         CK(cudaSetDevice(x->device));
         k_design_scalars<<<1, 32, 0, x->stream>>>(d.np, u, x->dscal);
-        k_design_update<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(x->g, d.np, u, x->dscal, x->gc,
-                                                                           x->region_mask, x->phases);
+        const int nbu = blocks_for(owned_nodes(x));
+        switch (d.np) {
+#define PETTO_UPD(NP)                                                                                   \
+    case NP:                                                                                            \
+        k_design_update<NP><<<nbu, 256, 0, x->stream>>>(x->g, u, x->dscal, x->gc, x->region_mask, x->phases); \
+        break;
+            PETTO_UPD(1) PETTO_UPD(2) PETTO_UPD(3) PETTO_UPD(4) PETTO_UPD(5) PETTO_UPD(6) PETTO_UPD(7) PETTO_UPD(8)
+#undef PETTO_UPD
+        }
         x->launches += 2;
         if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "design update launch failed");
         x->phi_ghosts_stale = true;
@@ -2156,6 +2231,35 @@ int team_ch_step(Team t, const petto_ch_params* p, petto_ch_stats* stats) {
     for (int q = 0; q < ctx->mat.nphases; ++q) {
         auto phi = [q](petto_ctx* x) { return x->phases + q * x->g.Ns; };
         auto slot = [q](int k) { return [q, k](petto_ctx* x) { return x->dscal + DS_CH + 3 * q + k; }; };
+        if (!t.replica()) {
+            // FAST: two passes per phase -- mu + mass before, then update + clamp +
+            // both masses -- with the sums as block partials (bit-identical to the
+            // term-array route, a third of the HBM traffic)
+            auto part = [](int k) { return [k](petto_ctx* x) { return x->pmax + k * x->npartials; }; };
+            if (t.split())
+                if (int rc = team_halo(t, phi, 1)) return rc;
+            for (int i = 0; i < t.n; ++i) {
+                petto_ctx* x = t.c[i];
+                CK(cudaSetDevice(x->device));
+                k_chem_potential_mass<<<sum_grid(x), 256, 0, x->stream>>>(x->g, phi(x), p->gamma, x->scratch1,
+                                                                           part(0)(x));
+                x->launches++;
+            }
+            if (int rc = team_sum_partials(t, part(0), sum_grid, slot(0))) return rc;
+            if (t.split())
+                if (int rc = team_halo(t, [](petto_ctx* x) { return x->scratch1; }, 1)) return rc;
+            for (int i = 0; i < t.n; ++i) {
+                petto_ctx* x = t.c[i];
+                CK(cudaSetDevice(x->device));
+                k_ch_update_clamp<<<sum_grid(x), 256, 0, x->stream>>>(x->g, x->scratch1, step, phi(x), part(1)(x),
+                                                                       part(2)(x), &x->status->flags);
+                x->launches++;
+                if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "cahn-hilliard launch failed");
+            }
+            if (int rc = team_sum_partials(t, part(1), sum_grid, slot(1))) return rc;
+            if (int rc = team_sum_partials(t, part(2), sum_grid, slot(2))) return rc;
+            continue;
+        }
         for (int i = 0; i < t.n; ++i) {
             petto_ctx* x = t.c[i];
             CK(cudaSetDevice(x->device));
@@ -2218,8 +2322,12 @@ int team_objectives(Team t, petto_report* rep, double* separation) {
         petto_ctx* x = t.c[i];
         CK(cudaSetDevice(x->device));
         CK(cudaMemsetAsync(x->count, 0, sizeof(unsigned long long), x->stream));
-        k_objective_terms<<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(
-            x->g, design_params(x), x->mat.kind, cl, cm, x->phases, x->st[x->cur], x->term1, x->term2, x->count);
+        if (x->g.dim == 3)
+            k_objective_terms<3><<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(
+                x->g, design_params(x), x->mat.kind, cl, cm, x->phases, x->st[x->cur], x->term1, x->term2, x->count);
+        else
+            k_objective_terms<2><<<blocks_for(owned_nodes(x)), 256, 0, x->stream>>>(
+                x->g, design_params(x), x->mat.kind, cl, cm, x->phases, x->st[x->cur], x->term1, x->term2, x->count);
         x->launches++;
         if (cudaGetLastError() != cudaSuccess) return fail(x, PETTO_ERROR, "objective launch failed");
     }
