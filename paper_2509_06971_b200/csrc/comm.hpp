@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <string>
 
 namespace petto_b200 {
@@ -34,8 +35,11 @@ struct NcclApi {
 
     bool load(std::string& err) {
         if (handle) return true;
-        // prefer an NCCL already mapped into the process (torch's), then the loader path
-        handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        // PETTO_NCCL_LIB names another libnccl-compatible library (the tests' in-process
+        // multi-rank emulator); otherwise prefer an NCCL already mapped into the process
+        // (torch's), then the loader path
+        if (const char* lib = std::getenv("PETTO_NCCL_LIB")) handle = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
+        if (!handle) handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
         if (!handle) handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!handle) handle = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!handle) {

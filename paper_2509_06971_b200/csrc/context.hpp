@@ -105,6 +105,9 @@ struct petto_ctx {
     double* pmax = nullptr;        // per-block maxima [blocks][8]
     unsigned long long* count = nullptr;
     double* dscal = nullptr;       // device scalars for the design kernels
+    double* hpin = nullptr;        // pinned host scratch (1024 doubles) for the small reads/writes:
+                                   // no pageable copy (it may serialise against other threads'
+                                   // CUDA calls while a stream waits on another rank)
 
     // peer halo (fused 3D steps write their boundary planes straight into the
     // neighbours' ghost planes; stream memory operations order the steps)

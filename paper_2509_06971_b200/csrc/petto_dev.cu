@@ -1090,7 +1090,9 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
         cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
-        cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess)
+        cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess ||
+        cudaMallocHost(&ctx->hpin, sizeof(double) * 1024) != cudaSuccess ||
+        cudaMalloc(&ctx->Kdev, sizeof(double) * 576) != cudaSuccess)
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
 #define E3_KERNEL e3::k_elastic3d_fast
@@ -1143,6 +1145,7 @@ void petto_dev_destroy(petto_ctx* ctx) {
     cudaFree(ctx->partials);
     cudaFree(ctx->status);
     cudaFree(ctx->dscal);
+    if (ctx->hpin) cudaFreeHost(ctx->hpin);
     if (ctx->status_h) cudaFreeHost(ctx->status_h);
     for (int b = 0; b < 2; ++b) {
         cudaFree(ctx->wtext[b]);
@@ -1324,7 +1327,10 @@ int petto_dev_init_operator(petto_ctx* ctx) {
         double e0 = ctx->prop_node0;
         if (!ctx->prop_node0_valid) {
             if (ctx->g.kb != 0) return fail(ctx, PETTO_INVALID, "node 0 property unknown on this rank");
-            CK(cudaMemcpy(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(ctx->hpin, ctx->prop + lidx(ctx->g, 0, 0, 0), sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            e0 = ctx->hpin[0];
         }
         l0 = cl * e0;
         m0 = cm * e0;
@@ -1337,9 +1343,11 @@ int petto_dev_init_operator(petto_ctx* ctx) {
     } catch (const std::exception& e) {
         return fail(ctx, PETTO_ERROR, e.what());
     }
-    cudaFree(ctx->Kdev);
-    CK(cudaMalloc(&ctx->Kdev, sizeof(double) * ctx->K.size()));
-    CK(cudaMemcpy(ctx->Kdev, ctx->K.data(), sizeof(double) * ctx->K.size(), cudaMemcpyHostToDevice));
+    // Kdev (576 doubles, allocated with the context): no allocation here -- this runs
+    // inside run(), where a device-synchronising call could wait on another rank
+    std::memcpy(ctx->hpin, ctx->K.data(), sizeof(double) * ctx->K.size());
+    CK(cudaMemcpyAsync(ctx->Kdev, ctx->hpin, sizeof(double) * ctx->K.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     ctx->op_ready = true;
     return PETTO_OK;
 }
@@ -2123,11 +2131,12 @@ int team_init_operator(Team t) {
                                                           ncclDouble, 0, static_cast<ncclComm_t>(ctx->nccl_comm),
                                                           ctx->stream), "node-0 broadcast"))
                 return rc;
-            CK(cudaMemcpyAsync(&e0, ctx->dscal + DS_CHAIN_IN, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(ctx->hpin, ctx->dscal + DS_CHAIN_IN, 8, cudaMemcpyDeviceToHost, ctx->stream));
         } else {
-            CK(cudaMemcpyAsync(&e0, ctx->prop + lidx(ctx->g, 0, 0, 0), 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(ctx->hpin, ctx->prop + lidx(ctx->g, 0, 0, 0), 8, cudaMemcpyDeviceToHost, ctx->stream));
         }
         CK(cudaStreamSynchronize(ctx->stream));
+        e0 = ctx->hpin[0];
         for (int i = 0; i < t.n; ++i) {
             t.c[i]->prop_node0 = e0;
             t.c[i]->prop_node0_valid = true;
@@ -2295,7 +2304,7 @@ int team_ch_step(Team t, const petto_ch_params* p, petto_ch_stats* stats) {
     }
     for (int i = 0; i < t.n; ++i) t.c[i]->phi_ghosts_stale = true;
     if (stats) {
-        double h[3 * PETTO_MAX_PHASES];
+        double* h = ctx->hpin;
         CK(cudaSetDevice(ctx->device));
         CK(cudaMemcpyAsync(h, ctx->dscal + DS_CH, sizeof(double) * 3 * ctx->mat.nphases, cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -2340,12 +2349,13 @@ int team_objectives(Team t, petto_report* rep, double* separation) {
     if (int rc = team_reduce(t, [](petto_ctx* x) -> void* { return x->count; }, 1, RED_SUM_U64)) return rc;
     if (int rc = team_phase_masses(t, DS_TMP)) return rc;
     if (int rc = team_region_sums(t)) return rc;
-    double h[DS_COUNT];
-    unsigned long long cnt = 0;
+    double* h = ctx->hpin;
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(h, ctx->dscal, sizeof(double) * DS_COUNT, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&cnt, ctx->count, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(h + DS_COUNT, ctx->count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    unsigned long long cnt;
+    std::memcpy(&cnt, h + DS_COUNT, sizeof(cnt));
     // scalar parts on the host, as the reference forms them
     const double inv_vol = 1.0 / domain_volume(ctx);
     petto_report r{};
