@@ -260,6 +260,8 @@ int petto_dev_peer_import(petto_ctx* ctx, const void* lo_blob, const void* hi_bl
 int petto_dev_group_link(petto_ctx** ctxs, int n);
 int petto_dev_group_hybrid_solve(petto_ctx** ctxs, int n, const petto_pt_params* p, int64_t* abort_step);
 int petto_dev_group_residual(petto_ctx** ctxs, int n, double* r_pde);
+int petto_dev_group_iterate_to_tolerance(petto_ctx** ctxs, int n, int mode, const petto_pt_params* p,
+                                         double target, long max_iters, petto_solve_stats* stats);
 int petto_dev_group_interpolate(petto_ctx** ctxs, int n);
 int petto_dev_group_init_operator(petto_ctx** ctxs, int n); /* nu from node 0 on the first slab */
 int petto_dev_group_design_update(petto_ctx** ctxs, int n);

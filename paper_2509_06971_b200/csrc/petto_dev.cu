@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -1512,62 +1513,6 @@ static int validate_params(petto_ctx* ctx, const petto_pt_params* p) {
     return PETTO_OK;
 }
 
-int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_params* p, double target,
-                                   long max_iters, petto_solve_stats* stats) {
-    CK(cudaSetDevice(ctx->device));
-    if (int rc = require_ready(ctx)) return rc;
-    if (int rc = check_kappa(ctx)) return rc;
-    if (int rc = reset_status(ctx)) return rc;
-    ctx->status_h->target = target;
-    ctx->status_h->max_iters = max_iters;
-    CK(cudaMemcpyAsync(ctx->status, ctx->status_h, sizeof(DeviceStatus), cudaMemcpyHostToDevice, ctx->stream));
-    const int spare = 3 - ctx->cur - ctx->prev;
-    const int b[3] = {ctx->cur, spare, ctx->prev};  // u_k lives in b[k % 3]
-    const StepCoef k = mode == 0 ? coef(2, p->dt_pt, p->theta) : coef(p->form ? 1 : 0, p->dt_apt, p->theta);
-    const long long never = LLONG_MAX;
-    long long launched = 0;  // residual evaluations issued
-    long long chunk = 32;
-    while (true) {
-        for (long long c = 0; c < chunk && launched <= max_iters; ++c, ++launched) {
-            const long long it = launched;
-            if (int rc = state_step(ctx, k, b[it % 3], b[(it + 2) % 3], ctx->st[b[(it + 1) % 3]], it + 1, never,
-                                    true))
-                return rc;
-            if (ctx->nccl_comm) {
-                // global r^2: local sum, all-reduce, then the stop test on every rank
-                if (ctx->mode == PETTO_MODE_FAST) {
-                    k_sum_to<<<1, 256, 0, ctx->stream>>>(ctx->partials, ctx->npartials_used, &ctx->status->sumsq);
-                    ctx->launches++;
-                }
-                if (int rc = allreduce(ctx, &ctx->status->sumsq, 1, ncclDouble, ncclSum)) return rc;
-                k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status, nullptr, 0);
-                if (int rc = halo(ctx, F_STATE, b[(it + 1) % 3])) return rc;
-            } else {
-                k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status,
-                                                          ctx->mode == PETTO_MODE_FAST ? ctx->partials : nullptr,
-                                                          ctx->npartials_used);
-            }
-            ctx->launches++;
-            CKL();
-        }
-        if (int rc = read_status(ctx)) return rc;
-        if (ctx->status_h->done || launched > max_iters) break;
-        chunk = std::min<long long>(chunk * 2, 4096);
-    }
-    const DeviceStatus& s = *ctx->status_h;
-    const long long n = s.iterations;
-    ctx->cur = b[n % 3];
-    ctx->prev = b[(n + 2) % 3];
-    stats->iterations = (long)n;
-    stats->r_initial = s.r_initial;
-    stats->r_final = s.r_final;
-    stats->converged = s.converged;
-    if (s.aborted)
-        return fail(ctx, PETTO_ABORT,
-                    "numerical abort in 'state' at step " + std::to_string(n) + ": residual norm diverged");
-    return PETTO_OK;
-}
-
 // ---------------------------------------------------------------- design (a19-a26)
 
 // MaterialModel::validate (objectives.hpp:26-33) / ObjectiveWeights::validate (:44-51)
@@ -2032,6 +1977,105 @@ int team_residual(Team t, double* r_pde) {
     return PETTO_OK;
 }
 
+// iterate_to_tolerance (state_solver.hpp:511-541): step, re-evaluate the residual,
+// stop below the absolute target -- the stop test on the device (k_iter_finish),
+// the host reading the status once per chunk of steps.  On slabs the r^2 of every
+// step is reduced over the slabs (REPLICA: the serial sum chained across them) and
+// the new state's ghost planes are exchanged before the next step.
+int team_iterate_to_tolerance(Team t, int mode, const petto_pt_params* p, double target, long max_iters,
+                              petto_solve_stats* stats) {
+    if (int rc = team_check(t)) return rc;
+    for (int i = 0; i < t.n; ++i) {
+        petto_ctx* ctx = t.c[i];
+        CK(cudaSetDevice(ctx->device));
+        if (int rc = require_ready(ctx)) return rc;
+        if (int rc = check_kappa(ctx)) return rc;
+        if (int rc = reset_status(ctx)) return rc;
+        ctx->status_h->target = target;
+        ctx->status_h->max_iters = max_iters;
+        CK(cudaMemcpyAsync(ctx->status, ctx->status_h, sizeof(DeviceStatus), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    petto_ctx* ctx = t.lead();
+    // u_k lives in b[k % 3] (the same rotation on every slab)
+    std::vector<std::array<int, 3>> b(t.n);
+    for (int i = 0; i < t.n; ++i) b[i] = {t.c[i]->cur, 3 - t.c[i]->cur - t.c[i]->prev, t.c[i]->prev};
+    const StepCoef k = mode == 0 ? coef(2, p->dt_pt, p->theta) : coef(p->form ? 1 : 0, p->dt_apt, p->theta);
+    const long long never = LLONG_MAX;
+    auto sumsq = [](petto_ctx* x) -> double* { return &x->status->sumsq; };
+    long long launched = 0;  // residual evaluations issued
+    long long chunk = 32;
+    while (true) {
+        for (long long c = 0; c < chunk && launched <= max_iters; ++c, ++launched) {
+            const long long it = launched;
+            for (int i = 0; i < t.n; ++i) {
+                petto_ctx* x = t.c[i];
+                CK(cudaSetDevice(x->device));
+                if (int rc = state_step(x, k, b[i][it % 3], b[i][(it + 2) % 3], x->st[b[i][(it + 1) % 3]], it + 1,
+                                        never, true))
+                    return rc;
+            }
+            if (!t.split()) {  // one domain: the partials straight into the stop test
+                k_iter_finish<<<1, 256, 0, ctx->stream>>>(ctx->status, t.replica() ? nullptr : ctx->partials,
+                                                          ctx->npartials_used);
+                ctx->launches++;
+                CKL();
+                continue;
+            }
+            if (t.replica()) {
+                if (int rc = team_chain(
+                        t, ctx->comps,
+                        [](petto_ctx* ctx, int cc, const double* init, double* out) {
+                            k_sumsq_serial<<<1, 32, 0, ctx->stream>>>(ctx->g, ctx->comps, ctx->r, out, cc, init);
+                            ctx->launches++;
+                            CKL();
+                            return PETTO_OK;
+                        },
+                        sumsq))
+                    return rc;
+            } else {
+                for (int i = 0; i < t.n; ++i) {
+                    petto_ctx* x = t.c[i];
+                    CK(cudaSetDevice(x->device));
+                    k_sum_to<<<1, 256, 0, x->stream>>>(x->partials, x->npartials_used, &x->status->sumsq);
+                    x->launches++;
+                }
+                if (int rc = team_reduce(t, [&](petto_ctx* x) -> void* { return sumsq(x); }, 1, RED_SUM)) return rc;
+            }
+            for (int i = 0; i < t.n; ++i) {
+                petto_ctx* x = t.c[i];
+                CK(cudaSetDevice(x->device));
+                k_iter_finish<<<1, 256, 0, x->stream>>>(x->status, nullptr, 0);
+                x->launches++;
+                CKL();
+            }
+            // the new state's ghost planes (u_{it+1} lives in b[(it+1) % 3])
+            for (int i = 0; i < t.n; ++i) t.c[i]->cur = b[i][(it + 1) % 3];
+            if (int rc = team_halo(t, [](petto_ctx* x) { return x->st[x->cur]; }, t.lead()->comps)) return rc;
+        }
+        CK(cudaSetDevice(ctx->device));
+        if (int rc = read_status(ctx)) return rc;
+        if (ctx->status_h->done || launched > max_iters) break;
+        chunk = std::min<long long>(chunk * 2, 4096);
+    }
+    const DeviceStatus s = *ctx->status_h;
+    const long long n = s.iterations;
+    for (int i = 0; i < t.n; ++i) {
+        t.c[i]->cur = b[i][n % 3];
+        t.c[i]->prev = b[i][(n + 2) % 3];
+    }
+    stats->iterations = (long)n;
+    stats->r_initial = s.r_initial;
+    stats->r_final = s.r_final;
+    stats->converged = s.converged;
+    if (s.aborted) {
+        for (int i = 0; i < t.n; ++i)
+            fail(t.c[i], PETTO_ABORT,
+                 "numerical abort in 'state' at step " + std::to_string(n) + ": residual norm diverged");
+        return PETTO_ABORT;
+    }
+    return PETTO_OK;
+}
+
 // ------------------------------------------------------------ design loop
 
 int team_require_design(Team t, bool need_state) {
@@ -2492,6 +2536,18 @@ int petto_dev_hybrid_solve(petto_ctx* ctx, const petto_pt_params* p, int64_t* ab
     CK(cudaSetDevice(ctx->device));
     if (int rc = solo_ok(ctx, true)) return rc;
     return team_hybrid_solve(Team{&ctx, 1}, p, abort_step);
+}
+
+int petto_dev_iterate_to_tolerance(petto_ctx* ctx, int mode, const petto_pt_params* p, double target,
+                                   long max_iters, petto_solve_stats* stats) {
+    CK(cudaSetDevice(ctx->device));
+    if (int rc = solo_ok(ctx, false)) return rc;
+    return team_iterate_to_tolerance(Team{&ctx, 1}, mode, p, target, max_iters, stats);
+}
+
+int petto_dev_group_iterate_to_tolerance(petto_ctx** c, int n, int mode, const petto_pt_params* p, double target,
+                                         long max_iters, petto_solve_stats* stats) {
+    return team_iterate_to_tolerance(Team{c, n}, mode, p, target, max_iters, stats);
 }
 
 int petto_dev_residual(petto_ctx* ctx, double* out, double* r_pde) {

@@ -148,7 +148,7 @@ EXPORTED = [
     "petto_dev_design_update", "petto_dev_ch_step", "petto_dev_objectives", "petto_dev_run",
     "petto_dev_unit_cell_stiffness", "petto_dev_spectral_bound", "petto_dev_launch_count",
     "petto_dev_kernel_timing", "petto_dev_kernel_stats", "petto_dev_comm_unique_id", "petto_dev_comm_init",
-    "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_group_residual", "petto_dev_group_interpolate",
+    "petto_dev_group_link", "petto_dev_group_hybrid_solve", "petto_dev_group_residual", "petto_dev_group_iterate_to_tolerance", "petto_dev_group_interpolate",
     "petto_dev_group_init_operator",
     "petto_dev_group_design_update", "petto_dev_group_ch_step", "petto_dev_group_objectives", "petto_dev_group_run",
     "petto_dev_peer_export", "petto_dev_peer_import",
@@ -186,6 +186,14 @@ def group_residual(ctxs):
     r = C.c_double(0.0)
     ctxs[0]._check(lib().petto_dev_group_residual(_group(ctxs), len(ctxs), C.byref(r)))
     return r.value
+
+
+def group_iterate_to_tolerance(ctxs, mode, params, target, max_iters):
+    st = SolveStats()
+    ctxs[0]._check(lib().petto_dev_group_iterate_to_tolerance(_group(ctxs), len(ctxs), int(mode),
+                                                              C.byref(pt_params(params)), C.c_double(target),
+                                                              C.c_long(max_iters), C.byref(st)))
+    return st
 
 
 def group_interpolate(ctxs):

@@ -341,3 +341,45 @@ def test_group_abort_at_same_check_as_single_domain(mode):
     fin = np.isfinite(want)
     assert np.array_equal(np.isfinite(got), fin) and 0 < fin.sum() < fin.size
     assert np.array_equal(got[fin], want[fin])
+
+
+@pytest.mark.parametrize("mode", [D.MODE_REPLICA, D.MODE_FAST])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_group_iterate_to_tolerance(nranks, mode):
+    """iterate_to_tolerance (state_solver.hpp:511-541) on slabs: r^2 reduced over the
+    slabs every step (REPLICA chained: the same iteration count and state bit for
+    bit), the new state's ghost planes exchanged before the next step."""
+    g = P.Grid.make3d(33, 12, 14, 2.0, 1.0, 0.7)
+    comps, prop, src, bc, cur, prev = inputs(g, 1)
+    e, v = P.make_constraints(g, bc, comps)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.2 * h, theta=1.0, n_apt=30, n_pt=10, form=1)
+
+    def setup(ctx):
+        ctx.set_constraints(e, v)
+        ctx.set_source(src)
+        ctx.set_property(prop)
+        ctx.init_operator()
+        ctx.set_state(cur, prev)
+
+    one = D.Context(g, 1, 0.3, mode)
+    setup(one)
+    r0 = one.residual()[1]
+    setup(one)
+    want = one.iterate_to_tolerance(1, p, 0.2 * r0, 3000)
+    want_u = one.get_state()[0]
+    ctxs = [D.Context(g, 1, 0.3, mode, k_range=slab.slab_range(r, nranks, g.n[2])) for r in range(nranks)]
+    for c in ctxs:
+        setup(c)
+    D.group_link(ctxs)
+    got = D.group_iterate_to_tolerance(ctxs, 1, p, 0.2 * r0, 3000)
+    got_u = np.full(comps * g.num_nodes, np.nan)
+    for c in ctxs:
+        c.get_state(got_u, None)
+    assert got.converged == want.converged
+    if mode == D.MODE_REPLICA:
+        assert (got.iterations, got.r_initial, got.r_final) == (want.iterations, want.r_initial, want.r_final)
+        assert np.array_equal(got_u, want_u)
+    else:
+        assert abs(got.iterations - want.iterations) <= 1
+        assert abs(got.r_initial - want.r_initial) <= 1e-13 * want.r_initial
