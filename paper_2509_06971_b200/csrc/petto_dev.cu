@@ -31,6 +31,7 @@
 #include "writers.cuh"
 
 #include <cub/device/device_scan.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 using namespace petto_b200;
 
@@ -1638,6 +1639,16 @@ int petto_dev_get_phases(petto_ctx* ctx, double* phases) {
 // the single domain; FAST sums are per-slab trees plus one reduction.
 namespace {
 
+// NVTX range over one phase of the path (header-only NVTX v3: free unless a
+// profiler attaches) -- nsys / ncu timelines show hybrid_solve, the design-loop
+// phases, the halo exchanges and the slab reductions by name.
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+    Range(const Range&) = delete;
+    Range& operator=(const Range&) = delete;
+};
+
 struct Team {
     petto_ctx** c;
     int n;
@@ -1695,6 +1706,7 @@ constexpr int TEAM_MAX = 64;
 
 // in-place reduction of `count` device values at at(ctx) over the slabs
 int team_reduce(Team t, const PtrOf& at, int count, int op) {
+    Range nv("petto.team_reduce");
     const size_t es = op == RED_MAX_U32 ? 4 : 8;
     if (t.n == 1) {
         petto_ctx* ctx = t.c[0];
@@ -1731,6 +1743,7 @@ int team_reduce(Team t, const PtrOf& at, int count, int op) {
 using SegFn = std::function<int(petto_ctx*, int, const double*, double*)>;
 
 int team_chain(Team t, int nseg, const SegFn& seg, const DblOf& dst) {
+    Range nv("petto.team_chain");
     petto_ctx* ctx = t.lead();
     const bool ranks = t.nccl() && ctx->nranks > 1;
     if (t.n == 1 && !ranks) {
@@ -1833,6 +1846,7 @@ int sum_grid(const petto_ctx* ctx) { return (int)std::min<long long>(ctx->nparti
 
 // Ghost planes of `comps` fields starting at f(ctx) (component stride Ns).
 int team_halo(Team t, const DblOf& f, int comps) {
+    Range nv("petto.halo");
     if (t.n == 1) return t.nccl() ? halo_ptr(t.lead(), f(t.lead()), comps) : PETTO_OK;
     if (int rc = team_sync(t)) return rc;
     for (int i = 0; i < t.n; ++i) {
@@ -1863,6 +1877,7 @@ int team_phase_ghosts(Team t) {
 // ------------------------------------------------------------ state solver
 
 int team_hybrid_solve(Team t, const petto_pt_params* p, int64_t* abort_step) {
+    Range nv("petto.hybrid_solve");
     if (int rc = team_check(t)) return rc;
     for (int i = 0; i < t.n; ++i) {
         petto_ctx* ctx = t.c[i];
@@ -1939,6 +1954,7 @@ int team_hybrid_solve(Team t, const petto_pt_params* p, int64_t* abort_step) {
 
 // residual + residual_norm (state_solver.hpp:49-58, 327-385): sqrt(sum r^2) / N
 int team_residual(Team t, double* r_pde) {
+    Range nv("petto.residual");
     if (int rc = team_check(t)) return rc;
     for (int i = 0; i < t.n; ++i) {
         petto_ctx* ctx = t.c[i];
@@ -1985,6 +2001,7 @@ int team_residual(Team t, double* r_pde) {
 int team_iterate_to_tolerance(Team t, int mode, const petto_pt_params* p, double target, long max_iters,
                               petto_solve_stats* stats) {
     if (int rc = team_check(t)) return rc;
+    Range nv("petto.iterate_to_tolerance");
     for (int i = 0; i < t.n; ++i) {
         petto_ctx* ctx = t.c[i];
         CK(cudaSetDevice(ctx->device));
@@ -2144,6 +2161,7 @@ int team_region_sums(Team t) {
 // interpolate_into (objectives.hpp:95-116) over every stored plane (the ghost
 // planes too: the operator reads the property of the cells across a slab face)
 int team_interpolate(Team t) {
+    Range nv("petto.interpolate");
     if (int rc = team_require_design(t, false)) return rc;
     if (int rc = team_phase_ghosts(t)) return rc;
     for (int i = 0; i < t.n; ++i) {
@@ -2193,6 +2211,7 @@ int team_init_operator(Team t) {
 
 // sensitivities (objectives.hpp:336-439) + design_update_inplace (:444-480)
 int team_design_update(Team t) {
+    Range nv("petto.design_update");
     if (int rc = team_require_design(t, true)) return rc;
     petto_ctx* ctx = t.lead();
     const DesignP d = design_params(ctx);
@@ -2273,6 +2292,7 @@ int team_design_update(Team t) {
 // the owned planes from phi with fresh ghosts, phi += dt D lap(mu) with fresh mu
 // ghosts (the 2-plane footprint as two 1-plane exchanges), mass pre, clamp, mass post
 int team_ch_step(Team t, const petto_ch_params* p, petto_ch_stats* stats) {
+    Range nv("petto.ch_step");
     if (int rc = team_require_design(t, false)) return rc;
     petto_ctx* ctx = t.lead();
     // CahnHilliardParams::validate (phase_field.hpp:17-21)
@@ -2365,6 +2385,7 @@ int team_ch_step(Team t, const petto_ch_params* p, petto_ch_stats* stats) {
 // evaluate_objectives (objectives.hpp:304-320) + the separation metric
 // (optimizer.hpp:95-112) of the current design and state
 int team_objectives(Team t, petto_report* rep, double* separation) {
+    Range nv("petto.objectives");
     if (int rc = team_require_design(t, true)) return rc;
     petto_ctx* ctx = t.lead();
     const int np = ctx->mat.nphases;
@@ -2454,6 +2475,7 @@ int team_run(Team t, const petto_schedule* s, petto_record_cb cb, void* user, pe
     std::vector<petto_ch_stats> chs(ctx->mat.nphases);
     auto flags = [](petto_ctx* x) -> void* { return &x->status->flags; };
     for (long loop = 1; loop <= s->max_loops; ++loop) {
+        Range nv("petto.loop");
         res.loops = loop;
         if (int rc = team_interpolate(t)) return rc;
         int64_t astep = 0;

@@ -27,6 +27,17 @@ def test_header_symbols_exported():
     assert sorted(D.EXPORTED) == names
 
 
+def test_nvtx_ranges_compiled_in():
+    """the library names its phases as NVTX ranges (header-only
+    NVTX v3, free unless a profiler attaches) -- the strings are in the binary."""
+    from paper_2509_06971_b200 import build
+
+    blob = open(build.LIB, "rb").read()
+    for name in (b"petto.hybrid_solve", b"petto.iterate_to_tolerance", b"petto.loop", b"petto.design_update",
+                 b"petto.ch_step", b"petto.objectives", b"petto.halo", b"petto.team_reduce"):
+        assert name in blob, name
+
+
 def test_version_and_device_count():
     L = D.lib()
     assert b"sm_100a" in L.petto_dev_version()
