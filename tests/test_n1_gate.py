@@ -146,7 +146,7 @@ def test_elastic_iteration_count_at_c4(mode):
     ctx.init_operator()
     z = np.zeros(3 * prob.grid.num_nodes)
     ctx.set_state(z, z)
-    st = ctx.iterate_to_tolerance(1, sched.pt, d["target"], 40000)
+    st = ctx.iterate_to_tolerance(1, sched.pt, d["target"], 20000)
     print(f"C4 tolerance {mode}: {st.iterations} iterations (reference {d['iterations']}), "
           f"r_final {st.r_final:.6e} (reference {d['r_final']:.6e})")
     assert bool(st.converged) == bool(d["converged"])
