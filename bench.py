@@ -274,7 +274,6 @@ def run_ours(a):
     g = prob.grid
     N = g.num_nodes
     comps = prob.comps
-    # strong scaling: the C5 grid is slab-decomposed along its outermost axis
     # strong scaling: the grid is slab-decomposed along its outermost device axis --
     # x (the longest axis of the cantilever configs) in the x-outermost layout
     xo = a.layout == "x" or (a.layout == "auto" and g.dim == 3 and prob.physics == 1)
