@@ -53,6 +53,9 @@ def args_():
     a.add_argument("--layout", choices=["auto", "reference", "x"], default="auto",
                    help="device layout: x-outermost (slabs along x, the longest axis) or the reference's; "
                         "auto = x for 3D elasticity")
+    a.add_argument("--e2e-layout", choices=["auto", "reference", "x"], default="auto",
+                   help="device layout of the e2e contexts; auto = the reference layout on one GPU (host arrays "
+                        "upload without a permutation), the run's layout on slabs")
     a.add_argument("--no-cpu", action="store_true")
     a.add_argument("--cpu-steps", type=int, default=2, help="APT steps in the CPU baseline sample")
     return a.parse_args()
@@ -365,10 +368,14 @@ def run_ours(a):
     e2e = None
     if not a.no_e2e:
         pipe = max(1, a.e2e_pipeline) if world == 1 else 1
-        ctxs = [ctx]
-        for _ in range(pipe - 1):
+        # the e2e contexts' layout: on one GPU the reference's (the host arrays
+        # upload as plain copies; the permuting transposes of the x-outermost layout
+        # would compete for SMs with the other contexts' solves), on slabs the run's
+        e2e_xo = a.e2e_layout == "x" or (a.e2e_layout == "auto" and world > 1 and xo)
+        ctxs = [ctx] if e2e_xo == xo else []
+        while len(ctxs) < pipe:
             c2 = D.Context(g, prob.physics, prob.poisson_ratio, D.MODE_FAST, device=local, k_range=k_range,
-                           x_outermost=xo)
+                           x_outermost=e2e_xo)
             c2.set_constraints(prob.cons_entry, prob.cons_value)
             c2.set_source(prob.source)
             c2.set_property(E)
@@ -421,7 +428,8 @@ def run_ours(a):
         e2e = {"value": N * a.n_apt * e2e_steps / dt / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 2 * moved, "d2h_bytes_per_step": 2 * comps * N * 8,
                "steps": e2e_steps, "pipeline": f"{pipe} contexts from {pipe} host threads"
-               if pipe > 1 else "sequential"}
+               if pipe > 1 else "sequential",
+               "layout": "x-outermost" if e2e_xo else "reference (x fastest)"}
         if pipe > 1:
             # what one drop-in caller sees: one context, upload -> solve -> download in turn
             torch.cuda.synchronize()
