@@ -52,7 +52,8 @@ inline void check(petto_ctx* ctx, int rc, long long step = -1) {
 // One problem resident in HBM.
 class Context {
 public:
-    Context(const Grid& g, int physics, double nu, int mode = PETTO_MODE_FAST, int device = 0) {
+    Context(const Grid& g, int physics, double nu, int mode = PETTO_MODE_FAST, int device = 0,
+            bool x_outermost = false) {
         petto_grid_desc d{};
         d.dim = g.dim;
         for (int a = 0; a < 3; ++a) {
@@ -63,7 +64,13 @@ public:
         d.poisson_ratio = nu;
         d.mode = mode;
         d.device = device;
+        d.x_outermost = x_outermost ? 1 : 0;
         check(nullptr, petto_dev_create(&d, &ctx_));
+    }
+    // The device layout run() picks: x outermost for a FAST 3D elasticity grid whose
+    // longest axis is x (the cantilever configs; measured faster)
+    static bool prefer_x_outermost(const Grid& g, int physics, int mode) {
+        return g.dim == 3 && physics == 1 && mode == PETTO_MODE_FAST && g.n[0] >= g.n[1] && g.n[0] >= g.n[2];
     }
     ~Context() { petto_dev_destroy(ctx_); }
     Context(const Context&) = delete;
@@ -204,7 +211,7 @@ inline OptimizationResult<double> run(const Problem<double>& prob, const LoopSch
     const Grid& g = *prob.grid;
     const int physics = prob.kind == MaterialKind::Elastic ? 1 : 0;
     const int comps = physics ? g.dim : 1;
-    Context cx(g, physics, prob.material.poisson_ratio, mode);
+    Context cx(g, physics, prob.material.poisson_ratio, mode, 0, Context::prefer_x_outermost(g, physics, mode));
     petto_ctx* c = cx.get();
     const ConstraintSet cs = make_constraints(g, prob.bc, comps);
     check(c, petto_dev_set_constraints(c, cs.entry.data(), cs.value.data(), static_cast<int64_t>(cs.size())));
