@@ -142,6 +142,8 @@ struct petto_ctx {
     unsigned long long* cta_probe = nullptr;  // probe builds only (E3_CTA_TIMING)
     bool no_tblock = false;                   // PETTO_NO_TBLOCK=1: per-step grid barriers for 2D heat
     bool no_pdl = false;                      // PETTO_NO_PDL=1: plain stream order between fused 3D steps
+    int multi = -1;                           // PETTO_MULTI: persistent 3D solves (-1 auto, 0 off, 1 on)
+    unsigned* gbar = nullptr;                 // grid barrier counter of persistent launches
     long long launches = 0;
     bool timing = false;
     int timing_stride = 1;      // events around every timing_stride-th timed launch

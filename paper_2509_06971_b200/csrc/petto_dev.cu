@@ -574,6 +574,147 @@ FusedParams fused_params(const petto_ctx* ctx, const StepCoef& k, int cur, int p
     return P;
 }
 
+// The fused 3D elasticity step (k_elastic3d_fast): one step, or with nloc > 1 a
+// persistent launch of steps step .. step + nloc - 1 (single domain, output =
+// st[prev], no r^2 partials).
+int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, long long step,
+              long long nsteps, double* partials, int nloc) {
+    const Geo& g = ctx->g;
+    cudaEvent_t ev[2];
+    const long long owned = owned_nodes(ctx);
+    if (!ctx->tmaps && make_tmaps(ctx)) return PETTO_ERROR;
+    const double nu = ctx->desc.poisson_ratio;
+    const double e_scale =
+        (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
+    if (!ctx->ecell_valid || ctx->ecell_scale != e_scale) {
+        e3::k_cell_modulus<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(g, ctx->prop, e_scale, ctx->ecell);
+        ctx->launches++;
+        CKL();
+        ctx->ecell_valid = true;
+        ctx->ecell_scale = e_scale;
+    }
+    e3::Params P{};
+    P.g = g;
+    for (int i = 0; i < 45; ++i) P.kh[i] = ctx->kh[i];
+    P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
+    if (k.form == 0) {  // 2u - u_prev + a r - b (u - u_prev)
+        P.c1 = 2.0 - k.b;
+        P.c2 = 1.0 - k.b;
+        P.c3 = k.a;
+    } else if (k.form == 1) {  // (2u - u_prev + b u + a r) / (1 + b)
+        P.c1 = (2.0 + k.b) * k.inv;
+        P.c2 = k.inv;
+        P.c3 = k.a * k.inv;
+    }
+    P.dt = k.dt;
+    P.next = next;
+    if (ctx->peer_step) {
+        int ob = -1;
+        for (int b = 0; b < 3; ++b)
+            if (next == ctx->st[b]) ob = b;
+        if (ob < 0) return fail(ctx, PETTO_ERROR, "peer halo: output is not a state buffer");
+        const long long plane = (long long)g.px * g.ny;
+        if (ctx->peer_lo.st[0]) {
+            P.peer_lo = ctx->peer_lo.st[ob] + (long long)(g.ks0 - ctx->peer_lo.ks0) * plane;
+            P.peer_lo_Ns = ctx->peer_lo.Ns;
+        }
+        if (ctx->peer_hi.st[0]) {
+            P.peer_hi = ctx->peer_hi.st[ob] + (long long)(g.ks0 - ctx->peer_hi.ks0) * plane;
+            P.peer_hi_Ns = ctx->peer_hi.Ns;
+        }
+    }
+    P.aux = ctx->aux;
+#ifdef E3_CTA_TIMING
+    {
+        static unsigned long long* probe = nullptr;
+        if (!probe) cudaMalloc(&probe, sizeof(unsigned long long) * 4 * 1024);
+        P.cta_ns = probe;
+        ctx->cta_probe = probe;
+    }
+#endif
+    P.partials = partials;
+    P.status = ctx->status;
+    P.step = step;
+    P.nsteps = nsteps;
+    P.ntx = (g.nx + 31) / 32;
+    P.nstrips = (g.ny + e3::W - 1) / e3::W;
+    int grid = 0;
+    plan_3d(ctx, P.nstrips, P.chunk, P.nitems, grid);
+    if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
+    e3::MapSet<2> MS;
+    int ob = next == ctx->r ? 3 : -1;
+    for (int b = 0; b < 3; ++b)
+        if (next == ctx->st[b]) ob = b;
+    if (ob < 0) return fail(ctx, PETTO_ERROR, "fused 3D step: output is not a context buffer");
+    MS.m[0].u = ctx->tU[cur];
+    MS.m[0].c = ctx->tC;
+    MS.m[0].p = ctx->tP[prev];
+    MS.m[0].m = ctx->tM;
+    MS.m[0].o = ctx->tO[ob];
+    if (nloc > 1) {
+        // u_{n+1} overwrites u_{n-1}; the next step reads it as u_n
+        if (ob != prev || partials || ctx->peer_step) return fail(ctx, PETTO_ERROR, "persistent 3D launch: bad plan");
+        MS.m[1] = MS.m[0];
+        MS.m[1].u = ctx->tU[prev];
+        MS.m[1].p = ctx->tP[cur];
+        MS.m[1].o = ctx->tO[cur];
+        P.nloc = nloc;
+        P.gbar = ctx->gbar;
+        CK(cudaMemsetAsync(ctx->gbar, 0, sizeof(unsigned), ctx->stream));
+    }
+    const e3::MapSet<1>& M1 = *reinterpret_cast<const e3::MapSet<1>*>(&MS.m[0]);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(e3::WS_THREADS);
+    cfg.dynamicSmemBytes = e3::SMEM_BYTES;
+    cfg.stream = ctx->stream;
+    timing_begin(ctx, ev);
+    // Programmatic dependent launch: step s+1's CTAs become resident on the SMs
+    // step s leaves idle and finish their setup (TMEM, barriers, tensor maps)
+    // before griddepcontrol.wait releases them at step s's completion.  Only
+    // when the plan leaves SMs idle (C4: 110 of 148; at C5 every SM is busy
+    // and it measured 0.7% slower), not on a launch whose duration is sampled,
+    // and not on slab ranks, whose steps are separated by stream memory
+    // operations.
+    cudaLaunchAttribute la[1];
+    if (nloc > 1) {  // every CTA resident (the grid barrier), or the launch fails
+        la[0].id = cudaLaunchAttributeCooperative;
+        la[0].val.cooperative = 1;
+        cfg.attrs = la;
+        cfg.numAttrs = 1;
+    } else if (!ctx->no_pdl && !ctx->peer_step && grid < ctx->nsm && !ev[0]) {
+        la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        la[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = la;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t le;
+    // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
+    if (nloc > 1) {
+        switch (k.form) {
+            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false, 2>, P, MS); break;
+            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false, 2>, P, MS); break;
+            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false, 2>, P, MS); break;
+        }
+    } else
+    switch (k.form * 2 + (partials ? 1 : 0)) {
+        case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false, 1>, P, M1); break;
+        case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, true, 1>, P, M1); break;
+        case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false, 1>, P, M1); break;
+        case 3: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, true, 1>, P, M1); break;
+        case 4: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false, 1>, P, M1); break;
+        case 5: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, true, 1>, P, M1); break;
+        case 6: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, false, 1>, P, M1); break;
+        default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true, 1>, P, M1); break;
+    }
+    if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
+    timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * step_bytes(ctx, k.form) * nloc);
+    ctx->launches++;
+    CKL();
+    if (partials) ctx->npartials_used = grid;
+    return PETTO_OK;
+}
+
 // One fused (fast) or replica state step: reads st[cur] (and st[prev]), writes
 // `next` (a state buffer or the residual scratch for form 3).
 int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, long long step, long long nsteps,
@@ -583,117 +724,7 @@ int state_step(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* nex
     if (ctx->mode == PETTO_MODE_FAST) {
         cudaEvent_t ev[2];
         const long long owned = owned_nodes(ctx);
-        if (g.dim == 3 && ctx->desc.physics == 1) {
-            if (!ctx->tmaps && make_tmaps(ctx)) return PETTO_ERROR;
-            const double nu = ctx->desc.poisson_ratio;
-            const double e_scale =
-                (ctx->prop_is_mu ? 1.0 : 1.0 / (2.0 * (1.0 + nu))) * (2.0 * (1.0 + ctx->nu_op) / 8.0);
-            if (!ctx->ecell_valid || ctx->ecell_scale != e_scale) {
-                e3::k_cell_modulus<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(g, ctx->prop, e_scale, ctx->ecell);
-                ctx->launches++;
-                CKL();
-                ctx->ecell_valid = true;
-                ctx->ecell_scale = e_scale;
-            }
-            e3::Params P{};
-            P.g = g;
-            for (int i = 0; i < 45; ++i) P.kh[i] = ctx->kh[i];
-            P.inv_base = 1.0 / (g.h[0] * g.h[1] * g.h[2]);
-            if (k.form == 0) {  // 2u - u_prev + a r - b (u - u_prev)
-                P.c1 = 2.0 - k.b;
-                P.c2 = 1.0 - k.b;
-                P.c3 = k.a;
-            } else if (k.form == 1) {  // (2u - u_prev + b u + a r) / (1 + b)
-                P.c1 = (2.0 + k.b) * k.inv;
-                P.c2 = k.inv;
-                P.c3 = k.a * k.inv;
-            }
-            P.dt = k.dt;
-            P.next = next;
-            if (ctx->peer_step) {
-                int ob = -1;
-                for (int b = 0; b < 3; ++b)
-                    if (next == ctx->st[b]) ob = b;
-                if (ob < 0) return fail(ctx, PETTO_ERROR, "peer halo: output is not a state buffer");
-                const long long plane = (long long)g.px * g.ny;
-                if (ctx->peer_lo.st[0]) {
-                    P.peer_lo = ctx->peer_lo.st[ob] + (long long)(g.ks0 - ctx->peer_lo.ks0) * plane;
-                    P.peer_lo_Ns = ctx->peer_lo.Ns;
-                }
-                if (ctx->peer_hi.st[0]) {
-                    P.peer_hi = ctx->peer_hi.st[ob] + (long long)(g.ks0 - ctx->peer_hi.ks0) * plane;
-                    P.peer_hi_Ns = ctx->peer_hi.Ns;
-                }
-            }
-            P.aux = ctx->aux;
-#ifdef E3_CTA_TIMING
-            {
-                static unsigned long long* probe = nullptr;
-                if (!probe) cudaMalloc(&probe, sizeof(unsigned long long) * 4 * 1024);
-                P.cta_ns = probe;
-                ctx->cta_probe = probe;
-            }
-#endif
-            P.partials = partials;
-            P.status = ctx->status;
-            P.step = step;
-            P.nsteps = nsteps;
-            P.ntx = (g.nx + 31) / 32;
-            P.nstrips = (g.ny + e3::W - 1) / e3::W;
-            int grid = 0;
-            plan_3d(ctx, P.nstrips, P.chunk, P.nitems, grid);
-            if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
-            e3::Maps M;
-            M.u = ctx->tU[cur];
-            M.c = ctx->tC;
-            M.p = ctx->tP[prev];
-            M.m = ctx->tM;
-            {
-                int ob = next == ctx->r ? 3 : -1;
-                for (int b = 0; b < 3; ++b)
-                    if (next == ctx->st[b]) ob = b;
-                if (ob < 0) return fail(ctx, PETTO_ERROR, "fused 3D step: output is not a context buffer");
-                M.o = ctx->tO[ob];
-            }
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(e3::WS_THREADS);
-            cfg.dynamicSmemBytes = e3::SMEM_BYTES;
-            cfg.stream = ctx->stream;
-            timing_begin(ctx, ev);
-            // Programmatic dependent launch: step s+1's CTAs become resident on the SMs
-            // step s leaves idle and finish their setup (TMEM, barriers, tensor maps)
-            // before griddepcontrol.wait releases them at step s's completion.  Only
-            // when the plan leaves SMs idle (C4: 110 of 148; at C5 every SM is busy
-            // and it measured 0.7% slower), not on a launch whose duration is sampled,
-            // and not on slab ranks, whose steps are separated by stream memory
-            // operations.
-            cudaLaunchAttribute la[1];
-            if (!ctx->no_pdl && !ctx->peer_step && grid < ctx->nsm && !ev[0]) {
-                la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                la[0].val.programmaticStreamSerializationAllowed = 1;
-                cfg.attrs = la;
-                cfg.numAttrs = 1;
-            }
-            cudaError_t le;
-            // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
-            switch (k.form * 2 + (partials ? 1 : 0)) {
-                case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false>, P, M); break;
-                case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, true>, P, M); break;
-                case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false>, P, M); break;
-                case 3: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, true>, P, M); break;
-                case 4: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false>, P, M); break;
-                case 5: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, true>, P, M); break;
-                case 6: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, false>, P, M); break;
-                default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true>, P, M); break;
-            }
-            if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
-            timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * step_bytes(ctx, k.form));
-            ctx->launches++;
-            CKL();
-            if (partials) ctx->npartials_used = grid;
-            return PETTO_OK;
-        }
+        if (g.dim == 3 && ctx->desc.physics == 1) return e3_launch(ctx, k, cur, prev, next, step, nsteps, partials, 1);
         FusedParams P = fused_params(ctx, k, cur, prev, next, partials, step, nsteps);
         const int grid = (int)std::min<long long>(ctx->npartials, blocks_for(owned));
         timing_begin(ctx, ev);
@@ -1089,23 +1120,28 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
     ctx->npartials = std::max(32 * ctx->nsm, 1024);
     if (const char* e = std::getenv("PETTO_NO_TBLOCK")) ctx->no_tblock = e[0] == '1';  // A/B of the 2D solves
     if (const char* e = std::getenv("PETTO_NO_PDL")) ctx->no_pdl = e[0] == '1';        // A/B of the 3D step overlap
+    if (const char* e = std::getenv("PETTO_MULTI")) ctx->multi = e[0] - '0';          // A/B of persistent 3D solves
     if (cudaMalloc(&ctx->partials, sizeof(double) * ctx->npartials) != cudaSuccess ||
         cudaMalloc(&ctx->status, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMallocHost(&ctx->status_h, sizeof(DeviceStatus)) != cudaSuccess ||
         cudaMalloc(&ctx->dscal, sizeof(double) * 256) != cudaSuccess ||
         cudaMallocHost(&ctx->hpin, sizeof(double) * 1024) != cudaSuccess ||
-        cudaMalloc(&ctx->Kdev, sizeof(double) * 576) != cudaSuccess)
+        cudaMalloc(&ctx->Kdev, sizeof(double) * 576) != cudaSuccess ||
+        cudaMalloc(&ctx->gbar, sizeof(unsigned) * 32) != cudaSuccess)
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
 #define E3_KERNEL e3::k_elastic3d_fast
-    if (cudaFuncSetAttribute(E3_KERNEL<0, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<0, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<3, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<3, true>, smattr, e3::SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(E3_KERNEL<0, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<0, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<0, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");
@@ -1144,6 +1180,7 @@ void petto_dev_destroy(petto_ctx* ctx) {
     cudaFree(ctx->cons_ent);
     cudaFree(ctx->cons_val);
     cudaFree(ctx->Kdev);
+    cudaFree(ctx->gbar);
     cudaFree(ctx->partials);
     cudaFree(ctx->status);
     cudaFree(ctx->dscal);
@@ -1415,6 +1452,17 @@ int hybrid_step(petto_ctx* ctx, const StepCoef& k, long long step, long long nst
     std::swap(ctx->cur, ctx->prev);
     if (peer) return peer_signal(ctx, seq);
     return halo(ctx, F_STATE, ctx->cur);
+}
+
+// Persistent 3D elasticity solves (k_elastic3d_fast<., ., 2>): one domain, fast
+// mode, grids whose per-step launch overhead is not negligible (<= 16 M nodes,
+// e.g. C4); PETTO_MULTI=0/1 forces it off/on (A/B).
+bool persistent_3d_ok(const petto_ctx* ctx) {
+    const Geo& g = ctx->g;
+    if (ctx->mode != PETTO_MODE_FAST || g.dim != 3 || ctx->desc.physics != 1 || ctx->nccl_comm || ctx->nb_lo ||
+        ctx->nb_hi || ctx->peer_halo || ctx->multi == 0)
+        return false;
+    return ctx->multi == 1 || owned_nodes(ctx) <= (16LL << 20);
 }
 
 // Small grids of the heat / 2D-elasticity operators: the whole hybrid_solve runs
@@ -1895,6 +1943,16 @@ int team_hybrid_solve(Team t, const petto_pt_params* p, int64_t* abort_step) {
     if (t.n == 1 && small_solve_ok(ctx)) {
         if (int rc = small_solve(ctx, ka, kp, p->n_apt, p->n_pt)) return rc;
         if (nsteps % 2) std::swap(ctx->cur, ctx->prev);  // the kernel swapped nsteps times
+    } else if (t.n == 1 && persistent_3d_ok(ctx)) {
+        // one persistent launch per form segment (APT, then PT)
+        for (int seg = 0; seg < 2; ++seg) {
+            const long long n = seg ? p->n_pt : p->n_apt, s0 = seg ? p->n_apt + 1 : 1;
+            if (n <= 0) continue;
+            if (int rc = e3_launch(ctx, seg ? kp : ka, ctx->cur, ctx->prev, ctx->st[ctx->prev], s0, nsteps, nullptr,
+                                   (int)n))
+                return rc;
+            if (n % 2) std::swap(ctx->cur, ctx->prev);
+        }
     } else {
         for (long long step = 1; step <= nsteps; ++step) {
             const StepCoef& k = step <= p->n_apt ? ka : kp;

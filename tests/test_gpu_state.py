@@ -461,3 +461,75 @@ def test_boundary_uploads_independent_of_order(port, gi, mode):
         assert np.array_equal(outs[0], want)
     else:
         assert rel_err(outs[0], want) < 1e-12
+
+
+def _elastic3d_solve(g, E, f, bc, u0, up0, p, multi):
+    """hybrid_solve of a 3D elasticity problem, FAST, one persistent launch per form
+    segment (PETTO_MULTI=1) or one launch per step (PETTO_MULTI=0)."""
+    import os
+
+    old = os.environ.get("PETTO_MULTI")
+    os.environ["PETTO_MULTI"] = "1" if multi else "0"
+    try:
+        op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=FAST)
+    finally:
+        if old is None:
+            del os.environ["PETTO_MULTI"]
+        else:
+            os.environ["PETTO_MULTI"] = old
+    hist = D.StateHistory(u0.copy(), up0.copy())
+    step = None
+    try:
+        D.hybrid_solve(hist, op, p)
+    except D.NumericalAbort as e:
+        step = e.step
+    return hist, step
+
+
+PERSISTENT_CASES = [
+    # grid, form, n_apt, n_pt
+    (P.Grid.make3d(70, 23, 19, 2.0, 1.0, 1.0), 1, 37, 24),    # several x tiles and strips, ragged
+    (P.Grid.make3d(12, 9, 10, 2.0, 1.0, 1.0), 0, 50, 0),
+    (P.Grid.make3d(40, 17, 130, 2.0, 1.0, 0.7), 0, 0, 33),   # several z chunks, pure PT
+    (P.Grid.make3d(128, 64, 64, 1.0, 1.0, 1.0), 1, 100, 100),  # C4's grid
+]
+
+
+@pytest.mark.parametrize("case", range(len(PERSISTENT_CASES)))
+def test_elastic3d_persistent_matches_per_step_solve(port, case):
+    """The persistent 3D solve (all steps of a form segment in one cooperative
+    launch, grid barriers between them) is bit-identical to one launch per step,
+    and agrees with the oracle."""
+    g, form, n_apt, n_pt = PERSISTENT_CASES[case]
+    E, u, up, f, bc = elastic_case(g, 4)
+    e, v = P.make_constraints(g, bc, 3)
+    u[e] = v
+    up[e] = v
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.05 * h, theta=1.0, n_apt=n_apt, n_pt=n_pt, form=form)
+    a, sa = _elastic3d_solve(g, E, f, bc, u, up, p, True)
+    b, sb = _elastic3d_solve(g, E, f, bc, u, up, p, False)
+    assert sa is None and sb is None
+    assert np.array_equal(a.current, b.current) and np.array_equal(a.previous, b.previous)
+    if g.num_nodes <= 40 * 17 * 130:
+        rc, wc, wp, _ = port.hybrid_solve(1, g, bc, E, 0.3, f, u, up, p)
+        assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
+
+
+@pytest.mark.parametrize("n_apt", [150, 230])
+def test_elastic3d_persistent_abort_state(n_apt):
+    """An exploding 3D solve aborts at the same check_finite step with the same
+    buffers in the persistent and the per-step solve (the steps after the check
+    are skipped inside the launch)."""
+    g = P.Grid.make3d(40, 17, 12, 2.0, 1.0, 0.7)
+    E = H.random_modulus(g, 2)
+    f = H.sparse_loads(g, 3, 3)
+    bc = H.elastic_bc(g, "x_hi")
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=40.0 * h, theta=1.0, n_apt=n_apt, n_pt=0, form=0)
+    u0 = H.random_field(3 * g.num_nodes, 9, -1e-3, 1e-3)
+    a, sa = _elastic3d_solve(g, E, f, bc, u0, u0, p, True)
+    b, sb = _elastic3d_solve(g, E, f, bc, u0, u0, p, False)
+    assert sa is not None and sa == sb
+    assert np.array_equal(a.current, b.current, equal_nan=True)
+    assert np.array_equal(a.previous, b.previous, equal_nan=True)
