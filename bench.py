@@ -268,11 +268,22 @@ def run_ours(a):
     from paper_2509_06971_b200 import slab
 
     rank, world, local = dist_env()
+    # one GPU per rank; more ranks than GPUs share them (only the one-GPU runs of
+    # the multi-rank path below do that)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    # the set-up and timing collectives of the ranks: NCCL.  PETTO_BENCH_DIST_BACKEND=gloo
+    # is for the one-GPU runs of the multi-rank path (tests/test_gpu_nccl_emu_mp.py:
+    # several ranks on one device, the solver's NCCL through PETTO_NCCL_LIB).
+    backend = os.environ.get("PETTO_BENCH_DIST_BACKEND", "nccl")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg, prob, sched, E = workload(a.config, D.spectral_bound)
     g = prob.grid
     N = g.num_nodes
@@ -292,7 +303,7 @@ def run_ours(a):
     if world > 1:
         # NCCL communicator of the slab ranks: rank 0's unique id, broadcast
         uid = D.comm_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=coll_dev)
         torch.distributed.broadcast(t, 0)
         ctx.comm_init(bytes(t.cpu().tolist()), rank, world)
         if a.halo == "peer":
@@ -343,7 +354,7 @@ def run_ours(a):
     ctx.kernel_timing(False)
     launches = ctx.launch_count() - launches0
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     total_updates = N * a.n_apt * a.steps  # strong scaling: the whole grid, all ranks together
@@ -419,7 +430,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device="cuda")
+            t = torch.tensor([dt], device=coll_dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
         # bytes copied by the whole job per step (each rank moves its planes + ghosts)
