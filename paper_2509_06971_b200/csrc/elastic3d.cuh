@@ -450,14 +450,258 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// NM = 1: one step per launch.  NM = 2: a persistent launch of P.nloc steps
-// (cooperative, single domain) separated by grid barriers -- the launch, the
-// CTA setup and the tail of every step but the last disappear (small grids such
-// as C4, where they are a quarter of the step).
-template <int FORM, bool RSQ, int NM>
+template <int FORM, bool RSQ>
 __global__ void __launch_bounds__(WS_THREADS, 1)
-    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ MapSet<NM> MS) {
-    static_assert(NM == 1 || !RSQ, "persistent launches carry no r^2 partials");
+    k_elastic3d_fast(const __grid_constant__ Params P, const __grid_constant__ Maps M) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const Geo& g = P.g;
+    // Programmatic dependent launch: the next step may launch now; this one waits
+    // until the previous step has completed and its stores are visible (a no-op
+    // without the launch attribute).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (skip_step(P.status, P.step, P.nsteps)) return;
+#ifdef E3_CTA_TIMING
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    double* sY = reinterpret_cast<double*>(smem + OFF_Y);
+    double* sX = reinterpret_cast<double*>(smem + OFF_X);
+    Cursor* pc = reinterpret_cast<Cursor*>(smem + OFF_CUR);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    if (w == 0) tmem_alloc(tslot, TMEM_COLS);
+    if (w == 8 && l == 0) {
+        prefetch_tmap(&M.u);
+        prefetch_tmap(&M.c);
+        prefetch_tmap(&M.p);
+        prefetch_tmap(&M.m);
+        prefetch_tmap(&M.o);
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        pc->item = blockIdx.x;
+        pc->t = 0;
+        pc->kk = 0;
+        pc->set(P);
+        for (int s = 0; s < S - 1 && pc->valid; ++s) {
+            issue<FORM>(P, *pc, smem, bars, s, M);
+            pc->next(P);
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = *tslot;
+    double rsq = 0.0;
+    unsigned bad = 0;
+
+    if (w < NWARP) {
+        // ------------------------------------------------------------ cell warps
+        regs_grow<REG_CELL>();
+        double Bc[4][3], top[4][3];
+        uint32_t st = 0, phase = 0, q = 0;
+        const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (w >> 2) * 64;
+        walk(P, [&](bool own, int, int, int, int, bool two) {
+            mbar_wait(&bars[st], phase);
+            const unsigned char* sb = smem + st * STAGE_BYTES;
+            const double* sc = reinterpret_cast<const double*>(sb + OFF_C) + w * 32 + l;
+            if (!own) {  // prologue: node planes ka-1, ka and cell plane ka-1
+                double B0[4][3], Yd[2][3];
+                forward(sb, 0, w, l, B0);
+                forward(sb, 1, w, l, Bc);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) top[q4][c] = 0.0;
+#ifndef E3_PROBE_NOPROLOGUE  // probe build (wrong results): no cell work in the prologue
+                cell<false>(P, B0, Bc, sc[0], top, Yd, nullptr);
+#endif
+            } else {
+                double* sYw = sY + (q & 1) * (NWARP * YS) + w * YS + l;
+                double B1[4][3], Y0[2][3], Y1[2][3];
+                forward(sb, 0, w, l, B1);
+                cell<true>(P, Bc, B1, sc[0], top, Y0, sYw);
+                if (two) {
+                    forward(sb, 1, w, l, Bc);
+                    cell<true>(P, B1, Bc, sc[NWARP * 32], top, Y1, sYw + 6 * 32);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) Y1[k / 3][k % 3] = 0.0;
+                }
+                if (w > 0) {  // the y-halo row's own sums are not needed
+                    const uint32_t ta = tq + (q & 1) * 32;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) {
+                        tmem_st1(ta + 2 * k, Y0[k / 3][k % 3]);
+                        tmem_st1(ta + 12 + 2 * k, Y1[k / 3][k % 3]);
+                    }
+                    tmem_wait_st();
+                }
+            }
+            tmem_fence_before();
+#ifdef E3_SLOT_TIMING  // probe: warp 1 of CTA 0 records when it reaches / leaves each barrier
+            unsigned long long t_arrive;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arrive));
+#endif
+            __syncthreads();  // task q's shares and sums are complete
+#ifdef E3_SLOT_TIMING
+            if (blockIdx.x == 0 && w == 1 && l == 0 && P.cta_ns && q < 1000) {
+                unsigned long long t_leave;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_leave));
+                P.cta_ns[1024 + 3 * q] = t_arrive;
+                P.cta_ns[1024 + 3 * q + 1] = t_leave;
+                P.cta_ns[1024 + 3 * q + 2] = own ? 1 : 0;
+            }
+#endif
+            ++q;
+            if (++st == S) {
+                st = 0;
+                phase ^= 1u;
+            }
+        });
+        __syncthreads();  // the node warps' last task
+    } else if (w == NWARP) {
+        // ------------------------------------------------------------- producer
+        regs_shrink<REG_NODE>();
+        uint32_t st = 0, q = 0;
+        // the node output of the previous task (stored once the node warps are done with it)
+        bool pown = false, ptwo = false;
+        int pi0 = 0, pj0 = 0, pk = 0;
+        auto store_prev = [&]() {
+            if (l == 0 && pown) {
+                const double* so = reinterpret_cast<const double*>(smem + OFF_O) + ((q - 1) & 1) * (ZP * OSTRIDE);
+                tma_store_4d(&M.o, so, pi0, pj0, pk, 0);
+                if (ptwo) tma_store_4d(&M.o, so + OSTRIDE, pi0, pj0, pk + 1, 0);
+                bulk_commit();
+            }
+        };
+        walk(P, [&](bool own, int s, int t, int, int kc, bool two) {
+            if (l == 0) bulk_wait_read_all();  // staging (q-2) & 1 is free before the node warps refill it
+            __syncthreads();  // cell warps done with task q, node warps with task q-1
+            if (l == 0 && pc->valid) {  // refill the stage of task q-1
+                issue<FORM>(P, *pc, smem, bars, st == 0 ? S - 1 : st - 1, M);
+                pc->next(P);
+            }
+            store_prev();
+            pown = own;
+            ptwo = two;
+            pi0 = t * 32;
+            pj0 = s * W;
+            pk = kc - g.ks0;
+            ++q;
+            if (++st == S) st = 0;
+        });
+        __syncthreads();
+        store_prev();
+        if (l == 0) bulk_wait_all();
+    } else {
+        // ------------------------------------------------------------ node warps
+        regs_shrink<REG_NODE>();
+        const int v = w - NWARP;  // row j0-1+v, v = 1..7
+        double ucar[3] = {0.0, 0.0, 0.0};
+        uint32_t st = 0, q = 0;
+        const uint32_t tq = tbase + ((32u * (w & 3)) << 16) + (v >> 2) * 64;
+        Tile T{};  // set at each x tile's prologue task
+        int ntile = 0;
+        unsigned exm = 0xffffffffu;
+        walk(P, [&](bool own, int s, int t, int ka, int kc, bool two) {
+            __syncthreads();  // the cell warps finished task q
+            tmem_fence_after();
+            const unsigned char* sb = smem + st * STAGE_BYTES;
+            const double* su = reinterpret_cast<const double*>(sb + OFF_U) + v * BOXX + l;  // plane 0, row v
+            if (!own) {
+                const int i = t * 32 + l, j = s * W - 1 + v;
+                T.upd = i < g.nx && j < g.ny;
+                const int ends = (i == 0 || i == g.nx - 1) + (j == 0 || j == g.ny - 1);
+                T.ninv = -P.inv_base * (double)(1 << ends);
+                T.ca = (FORM <= 1 ? P.c3 : FORM == 2 ? P.dt : 1.0) * T.ninv;
+                T.node0 = (long long)j * g.px + i;
+                // x-halo buffers alternate per tile of the CTA; the first tile of an
+                // item reads zeros (no cell to the left of x = 0)
+                T.xw = sX + (ntile & 1) * (LMAX * NWARP * 3) + v * 3;
+                T.xr = sX + ((ntile + 1) & 1) * (LMAX * NWARP * 3) + v * 3;
+                if (t == 0) {
+                    for (int k = l; k < LMAX * 3; k += 32) const_cast<double*>(T.xr)[(k / 3) * (NWARP * 3) + k % 3] = 0.0;
+                    __syncwarp();
+                }
+                ++ntile;
+            } else {
+                double Yv[12];
+                tmem_ld12(tq + (q & 1) * 32, Yv);
+                const double Y0[2][3] = {{Yv[0], Yv[1], Yv[2]}, {Yv[3], Yv[4], Yv[5]}};
+                const double Y1[2][3] = {{Yv[6], Yv[7], Yv[8]}, {Yv[9], Yv[10], Yv[11]}};
+                const double* below = sY + (q & 1) * (NWARP * YS) + (v - 1) * YS + l;
+                const unsigned char* mk = sb + OFF_M + (v - 1) * 32 + l;
+                const double* sp = reinterpret_cast<const double*>(sb + OFF_P) + (v - 1) * 32 + l;
+                double* so = reinterpret_cast<double*>(smem + OFF_O) + (q & 1) * (ZP * OSTRIDE) + (v - 1) * 32 + l;
+                auto planes = [&](auto zend) {
+                    constexpr bool ZE = decltype(zend)::value;
+                    node<FORM, RSQ, ZE>(P, T, kc, kc - ka, Y0, below, ucar, sp, mk[0], so, rsq, exm);
+                    if (two) {
+                        double u1[3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) u1[c] = su[c * USTRIDE];
+                        node<FORM, RSQ, ZE>(P, T, kc + 1, kc + 1 - ka, Y1, below + 6 * 32, u1, sp + W * 32,
+                                            mk[W * 32], so + OSTRIDE, rsq, exm);
+                    }
+                };
+#ifndef E3_PROBE_NONODE  // probe build (wrong results): node warps skip the node work
+                if (kc == 0 || kc + 1 >= g.nz - 1) planes(std::true_type{});
+                else planes(std::false_type{});
+#else
+                (void)planes;
+#endif
+                fence_async_smem();  // the staging is read by the producer's TMA store
+            }
+            // u_n of the next task's first node plane (stage plane 1)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ucar[c] = su[c * USTRIDE + UROWS * BOXX];
+            ++q;
+            if (++st == S) st = 0;
+        });
+        if (P.peer_lo || P.peer_hi) __threadfence_system();  // peer stores before the step's signal
+        bad = exm == 0;
+        __syncthreads();
+    }
+
+    // CTA reduction of r^2 (fixed order) and the non-finite flag
+    double* red = reinterpret_cast<double*>(smem + OFF_RED);
+    rsq = warp_sum(rsq);
+    bad = __any_sync(0xffffffffu, bad);
+    if (l == 0) red[w] = rsq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int k = 0; k < 2 * NWARP; ++k) sum += red[k];
+        if (P.partials) P.partials[blockIdx.x] = sum;
+    }
+    if (bad && l == 0) mark_bad(P.status, P.step);
+    if (w == 0) tmem_dealloc(tbase, TMEM_COLS);
+#ifdef E3_CTA_TIMING
+    if (threadIdx.x == 0 && P.cta_ns) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.cta_ns[3 * blockIdx.x] = t_start;
+        P.cta_ns[3 * blockIdx.x + 1] = t_end;
+        P.cta_ns[3 * blockIdx.x + 2] = smid;
+    }
+#endif
+}
+
+// The persistent variant: P.nloc steps in one cooperative launch (single domain,
+// no r^2 partials), separated by grid barriers -- the launch, the CTA setup and
+// the tail of every step but the last disappear (small grids such as C4).  The
+// same roles and task walk as k_elastic3d_fast, each role looping over the steps
+// (its register budget set once); a separate kernel because folding the step loop
+// into k_elastic3d_fast cost its single-step launches 5% more cycles at C5.
+template <int FORM>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    k_elastic3d_persist(const __grid_constant__ Params P, const __grid_constant__ MapSet<2> MS) {
+    constexpr int NM = 2;
+    constexpr bool RSQ = false;
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;

@@ -662,7 +662,6 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
         P.gbar = ctx->gbar;
         CK(cudaMemsetAsync(ctx->gbar, 0, sizeof(unsigned), ctx->stream));
     }
-    const e3::MapSet<1>& M1 = *reinterpret_cast<const e3::MapSet<1>*>(&MS.m[0]);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(e3::WS_THREADS);
@@ -692,23 +691,24 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
     // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
     if (nloc > 1) {
         switch (k.form) {
-            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false, 2>, P, MS); break;
-            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false, 2>, P, MS); break;
-            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false, 2>, P, MS); break;
+            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<0>, P, MS); break;
+            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<1>, P, MS); break;
+            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<2>, P, MS); break;
         }
     } else
     switch (k.form * 2 + (partials ? 1 : 0)) {
-        case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false, 1>, P, M1); break;
-        case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, true, 1>, P, M1); break;
-        case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false, 1>, P, M1); break;
-        case 3: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, true, 1>, P, M1); break;
-        case 4: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false, 1>, P, M1); break;
-        case 5: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, true, 1>, P, M1); break;
-        case 6: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, false, 1>, P, M1); break;
-        default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true, 1>, P, M1); break;
+        case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, false>, P, MS.m[0]); break;
+        case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<0, true>, P, MS.m[0]); break;
+        case 2: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, false>, P, MS.m[0]); break;
+        case 3: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<1, true>, P, MS.m[0]); break;
+        case 4: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, false>, P, MS.m[0]); break;
+        case 5: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<2, true>, P, MS.m[0]); break;
+        case 6: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, false>, P, MS.m[0]); break;
+        default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true>, P, MS.m[0]); break;
     }
     if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
-    timing_end(ctx, ev, "k_elastic3d_fast", (double)owned * step_bytes(ctx, k.form) * nloc);
+    timing_end(ctx, ev, nloc > 1 ? "k_elastic3d_persist" : "k_elastic3d_fast",
+               (double)owned * step_bytes(ctx, k.form) * nloc);
     ctx->launches++;
     CKL();
     if (partials) ctx->npartials_used = grid;
@@ -1131,17 +1131,17 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         return cleanup("out of device memory (scalars)");
     const cudaFuncAttribute smattr = cudaFuncAttributeMaxDynamicSharedMemorySize;
 #define E3_KERNEL e3::k_elastic3d_fast
-    if (cudaFuncSetAttribute(E3_KERNEL<0, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<0, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<3, false, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<3, true, 1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<0, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<1, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(E3_KERNEL<2, false, 2>, smattr, e3::SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(E3_KERNEL<0, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<0, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<1, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<2, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(E3_KERNEL<3, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<2>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");
@@ -1454,7 +1454,7 @@ int hybrid_step(petto_ctx* ctx, const StepCoef& k, long long step, long long nst
     return halo(ctx, F_STATE, ctx->cur);
 }
 
-// Persistent 3D elasticity solves (k_elastic3d_fast<., ., 2>): one domain, fast
+// Persistent 3D elasticity solves (e3::k_elastic3d_persist): one domain, fast
 // mode, grids whose per-step launch overhead is not negligible (<= 16 M nodes,
 // e.g. C4); PETTO_MULTI=0/1 forces it off/on (A/B).
 bool persistent_3d_ok(const petto_ctx* ctx) {
