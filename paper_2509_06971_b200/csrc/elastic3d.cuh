@@ -69,6 +69,16 @@ constexpr int OFF_P = OFF_C + r128(ZP * NWARP * 32 * 8);      // [3][ZP][W][32] 
 constexpr int OFF_M = OFF_P + r128(3 * ZP * W * 32 * 8);      // [ZP][W][32] u8
 constexpr int STAGE_BYTES = OFF_M + r128(ZP * W * 32);
 constexpr uint32_t BYTES_U = 3 * ZP * UROWS * BOXX * 8;
+// Traffic-attribution probes (wrong results, ncu only): load U boxes without the
+// y-halo rows (E3_PROBE_UROWS=7) and / or the x-halo columns (E3_PROBE_UBOXX=32).
+#ifndef E3_PROBE_UROWS
+#define E3_PROBE_UROWS (E3_W + 2)
+#endif
+#ifndef E3_PROBE_UBOXX
+#define E3_PROBE_UBOXX 34
+#endif
+constexpr int LROWS = E3_PROBE_UROWS, LBOXX = E3_PROBE_UBOXX;
+constexpr uint32_t BYTES_U_LOAD = 3 * ZP * LROWS * LBOXX * 8;
 constexpr uint32_t BYTES_C = ZP * NWARP * 32 * 8;
 constexpr uint32_t BYTES_P = 3 * ZP * W * 32 * 8;
 constexpr uint32_t BYTES_M = ZP * W * 32;
@@ -159,7 +169,7 @@ __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned
     unsigned char* st = smem + stage * STAGE_BYTES;
     const bool own = c.kk >= 1;
     const bool need_p = own && FORM <= 1;
-    const uint32_t bytes = BYTES_U + BYTES_C + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
+    const uint32_t bytes = BYTES_U_LOAD + BYTES_C + (own ? BYTES_M : 0) + (need_p ? BYTES_P : 0);
     if (E3_EXPERIMENT == 1) {
         mbar_arrive(&bars[stage]);
         return;
@@ -169,7 +179,7 @@ __device__ __forceinline__ void issue(const Params& P, const Cursor& c, unsigned
     // first cell plane of the task; the node planes loaded are kc+1, kc+2 for an
     // owned task and kc, kc+1 (= ka-1, ka) for the prologue
     const int kc = own ? c.ka + ZP * (c.kk - 1) : c.ka - 1;
-    tma_load_4d(st + OFF_U, &T.u, &bars[stage], i0, j0 - 1, kc + (own ? 1 : 0) - P.g.ks0, 0);
+    tma_load_4d(st + OFF_U, &T.u, &bars[stage], i0, j0 - 1 + (UROWS - LROWS) / 2, kc + (own ? 1 : 0) - P.g.ks0, 0);
     tma_load_3d(st + OFF_C, &T.c, &bars[stage], i0, j0 - 1, kc - P.g.ks0);
     if (own) {
         tma_load_3d(st + OFF_M, &T.m, &bars[stage], i0, j0, kc - P.g.ks0);

@@ -361,7 +361,7 @@ int make_tmaps(petto_ctx* ctx) {
         return fail(ctx, PETTO_ERROR, "out of device memory (cell modulus)");
     const cuuint64_t d4[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzs, 3};
     const cuuint64_t s4[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.px * g.ny * 8, (cuuint64_t)g.Ns * 8};
-    const cuuint32_t boxU[4] = {e3::BOXX, e3::UROWS, e3::ZP, 3};
+    const cuuint32_t boxU[4] = {e3::LBOXX, e3::LROWS, e3::ZP, 3};
     const cuuint32_t boxP[4] = {32, e3::W, e3::ZP, 3};
     const cuuint32_t one[4] = {1, 1, 1, 1};
     auto map4 = [&](CUtensorMap* m, double* base, const cuuint32_t* box) {
