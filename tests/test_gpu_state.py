@@ -492,6 +492,7 @@ PERSISTENT_CASES = [
     (P.Grid.make3d(12, 9, 10, 2.0, 1.0, 1.0), 0, 50, 0),
     (P.Grid.make3d(40, 17, 130, 2.0, 1.0, 0.7), 0, 0, 33),   # several z chunks, pure PT
     (P.Grid.make3d(128, 64, 64, 1.0, 1.0, 1.0), 1, 100, 100),  # C4's grid
+    (P.Grid.make3d(33, 1100, 6, 1.0, 0.5, 1.0), 1, 20, 7),    # 158 strips: several items per CTA and step
 ]
 
 
@@ -511,7 +512,7 @@ def test_elastic3d_persistent_matches_per_step_solve(port, case):
     b, sb = _elastic3d_solve(g, E, f, bc, u, up, p, False)
     assert sa is None and sb is None
     assert np.array_equal(a.current, b.current) and np.array_equal(a.previous, b.previous)
-    if g.num_nodes <= 40 * 17 * 130:
+    if g.num_nodes <= 33 * 1100 * 6:
         rc, wc, wp, _ = port.hybrid_solve(1, g, bc, E, 0.3, f, u, up, p)
         assert rc == 0 and rel_err(a.current, wc) < 1e-10 and rel_err(a.previous, wp) < 1e-10
 
