@@ -711,20 +711,11 @@ template <int FORM>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     k_elastic3d_persist(const __grid_constant__ Params P, const __grid_constant__ MapSet<2> MS) {
     constexpr int NM = 2;
-    constexpr bool RSQ = false;
+    constexpr bool RSQ = false;  // no r^2 partials (node() template argument)
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
-    // Programmatic dependent launch: the next step may launch now; this one waits
-    // until the previous step has completed and its stores are visible (a no-op
-    // without the launch attribute).
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (skip_step(P.status, P.step, P.nsteps)) return;
-#ifdef E3_CTA_TIMING
-    unsigned long long t_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-#endif
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
@@ -748,17 +739,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     const uint32_t tbase = *tslot;
     double rsq = 0.0;
     // Per step: the roles walk the same tasks (one CTA barrier each, plus one after
-    // the last); then the step's non-finite mark and, between the steps of a
-    // persistent launch, the grid barrier.  Each role loops over the steps itself
-    // (its register budget is set once, by setmaxnreg).
-    const int nloc = NM == 1 ? 1 : P.nloc;
+    // the last); then the step's non-finite mark and, between steps, the grid
+    // barrier.  Each role loops over the steps itself (its register budget is set
+    // once, by setmaxnreg).
+    const int nloc = P.nloc;
     auto skip = [&](int si) {  // uniform over the grid: marks in flight are for steps >= this one
-        return NM > 1 && si > 0 && skip_step(P.status, P.step + si, P.nsteps);
+        return si > 0 && skip_step(P.status, P.step + si, P.nsteps);
     };
     auto step_end = [&](int si, unsigned bad) {
         bad = __any_sync(0xffffffffu, bad);
         if (bad && l == 0) mark_bad(P.status, P.step + si);
-        if (NM > 1 && si + 1 < nloc) {
+        if (si + 1 < nloc) {
             __syncthreads();  // the CTA's marks and (producer) completed stores
             if (w == NWARP && l == 0) grid_barrier(P.gbar, (unsigned)(si + 1) * gridDim.x);
             __syncthreads();
@@ -838,7 +829,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // ------------------------------------------------------------- producer
         regs_shrink<REG_NODE>();
         for (int si = 0; si < nloc && !skip(si); ++si) {
-            const Maps& M = MS.m[NM == 1 ? 0 : (si & 1)];
+            const Maps& M = MS.m[si & 1];
             if (l == 0) {  // the first S-1 tasks of the step, from the ring position on
                 pc->item = blockIdx.x;
                 pc->t = 0;
@@ -953,31 +944,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
     }
 
-    // CTA reduction of r^2 (fixed order)
-    if (RSQ) {
-        double* red = reinterpret_cast<double*>(smem + OFF_RED);
-        rsq = warp_sum(rsq);
-        if (l == 0) red[w] = rsq;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double sum = 0.0;
-            for (int k = 0; k < 2 * NWARP; ++k) sum += red[k];
-            if (P.partials) P.partials[blockIdx.x] = sum;
-        }
-    }
     __syncthreads();
     if (w == 0) tmem_dealloc(tbase, TMEM_COLS);
-#ifdef E3_CTA_TIMING
-    if (threadIdx.x == 0 && P.cta_ns) {
-        unsigned long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        P.cta_ns[3 * blockIdx.x] = t_start;
-        P.cta_ns[3 * blockIdx.x + 1] = t_end;
-        P.cta_ns[3 * blockIdx.x + 2] = smid;
-    }
-#endif
 }
 
 // Cell modulus of every stored cell (i, j, k), k = ks0 + kl: the operator scale
