@@ -57,14 +57,14 @@ def test_rank_processes_match_single_domain(nranks, mode, layout, halo):
         assert d["records_max_rel"] <= 1e-12 and d["phases_max_abs"] <= 1e-12
 
 
-@pytest.mark.parametrize("halo", ["peer", "nccl"])
-def test_bench_two_ranks(halo):
-    """bench.py --gpus 2 as the driver launches it (torchrun, one process per rank):
-    x-slabs, the halo, max-over-ranks timing, the e2e leg, one JSON line.  Both
+@pytest.mark.parametrize("nranks,halo", [(2, "peer"), (2, "nccl"), (4, "peer")])
+def test_bench_ranks(nranks, halo):
+    """bench.py --gpus N as the driver launches it (torchrun, one process per rank):
+    x-slabs, the halo, max-over-ranks timing, the e2e leg, one JSON line.  The
     ranks share one GPU here, so the numbers are not a scaling measurement."""
-    d = torchrun(2, ["bench.py", "--gpus", "2", "--config", "C4", "--steps", "3", "--warmup", "3", "--no-cpu",
-                     "--halo", halo], {"PETTO_BENCH_DIST_BACKEND": "gloo"})
+    d = torchrun(nranks, ["bench.py", "--gpus", str(nranks), "--config", "C4", "--steps", "3", "--warmup", "3",
+                          "--no-cpu", "--halo", halo], {"PETTO_BENCH_DIST_BACKEND": "gloo"})
     print(d)
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
-    assert d["config"]["parallelism"].startswith("slab2")
+    assert d["n_gpus"] == nranks and d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["parallelism"].startswith(f"slab{nranks}")
     assert ("peer" in d["halo"]) == (halo == "peer")
