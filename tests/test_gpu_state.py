@@ -534,3 +534,25 @@ def test_elastic3d_persistent_abort_state(n_apt):
     assert sa is not None and sa == sb
     assert np.array_equal(a.current, b.current, equal_nan=True)
     assert np.array_equal(a.previous, b.previous, equal_nan=True)
+
+
+@pytest.mark.parametrize("mode", [REPLICA, FAST])
+@pytest.mark.parametrize("c", [0.9050125313283208, 0.982])
+def test_iterate_to_tolerance_divergence_abort(port, mode, c):
+    """A diverging tolerance loop (explicit PT beyond its stability limit) aborts at
+    the iteration whose residual norm is first non-finite (state_solver.hpp:531-533),
+    like the reference -- also when that iteration is a multiple of 100, the
+    hybrid solve's check_finite cadence (c = 0.905: the reference aborts at 200)."""
+    g = P.Grid.make2d(24, 24, 1.0, 1.0)
+    bc = P.BoundarySpec.all_faces(2, P.DIRICHLET)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h * c, dt_apt=h / 2, theta=1.0, form=0)
+    z = np.zeros(g.num_nodes)
+    one = np.ones(g.num_nodes)
+    rc, want, _, _ = port.iterate_to_tolerance(0, g, bc, one, 0.3, one, z, z, 0, p, 1e-30, 1000)
+    assert rc != 0
+    op = D.HeatOperator(g, one, one, bc, mode=mode)
+    hist = D.StateHistory.of(z)
+    with pytest.raises(D.NumericalAbort) as ei:
+        D.iterate_to_tolerance(hist, op, 0, p, 1e-30, 1000)
+    assert ei.value.step == want.iterations
