@@ -701,21 +701,31 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 #endif
 }
 
-// The persistent variant: P.nloc steps in one cooperative launch (single domain,
-// no r^2 partials), separated by grid barriers -- the launch, the CTA setup and
-// the tail of every step but the last disappear (small grids such as C4).  The
-// same roles and task walk as k_elastic3d_fast, each role looping over the steps
-// (its register budget set once); a separate kernel because folding the step loop
-// into k_elastic3d_fast cost its single-step launches 5% more cycles at C5.
-template <int FORM>
+// The persistent variant: P.nloc steps in one cooperative launch (single domain),
+// separated by grid barriers -- the launch, the CTA setup and the tail of every
+// step but the last disappear (small grids such as C4).  The same roles and task
+// walk as k_elastic3d_fast, each role looping over the steps (its register budget
+// set once); a separate kernel because folding the step loop into
+// k_elastic3d_fast cost its single-step launches 5% more cycles at C5.
+//   TOL = false: hybrid_solve's steps P.step .. (u_{n+1} overwrites u_{n-1}).
+//   TOL = true: iterate_to_tolerance's iterations it = P.step .. (u_it in
+//   MS.m[it % 3], u_{it+1} into a third buffer), each with its r^2 partials
+//   (double-buffered by iteration parity); after the grid barrier every CTA sums
+//   them in k_iter_finish's order and applies its stop test, so all stop at the
+//   same iteration with the status k_iter_finish would have written.
+template <int FORM, bool TOL>
 __global__ void __launch_bounds__(WS_THREADS, 1)
-    k_elastic3d_persist(const __grid_constant__ Params P, const __grid_constant__ MapSet<2> MS) {
-    constexpr int NM = 2;
-    constexpr bool RSQ = false;  // no r^2 partials (node() template argument)
+    k_elastic3d_persist(const __grid_constant__ Params P, const __grid_constant__ MapSet<TOL ? 3 : 2> MS) {
+    constexpr int NM = TOL ? 3 : 2;
+    constexpr bool RSQ = TOL;  // r^2 partials (node() template argument)
     extern __shared__ __align__(128) unsigned char smem[];
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const Geo& g = P.g;
-    if (skip_step(P.status, P.step, P.nsteps)) return;
+    if (TOL ? P.status->done != 0 : skip_step(P.status, P.step, P.nsteps)) return;
+    // the stop test's constants (iterate_to_tolerance)
+    const double target = P.status->target, nodes = P.status->nodes;
+    const long long max_iters = P.status->max_iters;
+    bool stop = false;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     double* sY = reinterpret_cast<double*>(smem + OFF_Y);
     double* sX = reinterpret_cast<double*>(smem + OFF_X);
@@ -744,12 +754,58 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // once, by setmaxnreg).
     const int nloc = P.nloc;
     auto skip = [&](int si) {  // uniform over the grid: marks in flight are for steps >= this one
-        return si > 0 && skip_step(P.status, P.step + si, P.nsteps);
+        return TOL ? stop : si > 0 && skip_step(P.status, P.step + si, P.nsteps);
     };
     auto step_end = [&](int si, unsigned bad) {
         bad = __any_sync(0xffffffffu, bad);
-        if (bad && l == 0) mark_bad(P.status, P.step + si);
-        if (si + 1 < nloc) {
+        const long long it = P.step + si;
+        if (bad && l == 0) mark_bad(P.status, TOL ? it + 1 : it);
+        if (TOL) {
+            // the CTA's r^2 partial, in k_elastic3d_fast's order
+            double* red = reinterpret_cast<double*>(smem + OFF_RED);
+            const double v = warp_sum(rsq);
+            rsq = 0.0;
+            if (l == 0) red[w] = v;
+            __syncthreads();
+            double* part = P.partials + (it & 1) * gridDim.x;
+            if (threadIdx.x == 0) {
+                double sum = 0.0;
+                for (int k = 0; k < 2 * NWARP; ++k) sum += red[k];
+                part[blockIdx.x] = sum;
+            }
+            __syncthreads();  // the partial and (producer) the completed stores
+            if (w == NWARP && l == 0) grid_barrier(P.gbar, (unsigned)(si + 1) * gridDim.x);
+            __syncthreads();
+            // k_iter_finish: 256 threads stride over the partials, block_sum<8>
+            if (w < 8) {
+                double x = 0.0;
+                for (int t = threadIdx.x; t < (int)gridDim.x; t += 256) x += __ldcg(part + t);
+                x = warp_sum(x);
+                if (l == 0) red[w] = x;
+            }
+            __syncthreads();
+            if (w == 0) {
+                double x = l < 8 ? red[l] : 0.0;
+                x = warp_sum(x);
+                if (l == 0) red[8] = x;
+            }
+            __syncthreads();
+            const double r = sqrt(red[8]) / nodes;
+            const bool first = it == 0;
+            const bool aborted = !first && !isfinite(r);
+            const bool converged = !aborted && r < target;
+            stop = aborted || converged || it >= max_iters;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                DeviceStatus* s = P.status;
+                if (first) s->r_initial = r;
+                else s->iterations = it;
+                s->r_final = r;
+                if (stop) s->done = 1;
+                if (converged) s->converged = 1;
+                if (aborted) s->aborted = 1;
+                s->iter = it + 1;
+            }
+        } else if (si + 1 < nloc) {
             __syncthreads();  // the CTA's marks and (producer) completed stores
             if (w == NWARP && l == 0) grid_barrier(P.gbar, (unsigned)(si + 1) * gridDim.x);
             __syncthreads();
@@ -829,7 +885,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // ------------------------------------------------------------- producer
         regs_shrink<REG_NODE>();
         for (int si = 0; si < nloc && !skip(si); ++si) {
-            const Maps& M = MS.m[si & 1];
+            const Maps& M = MS.m[TOL ? (P.step + si) % 3 : (si & 1)];
             if (l == 0) {  // the first S-1 tasks of the step, from the ring position on
                 pc->item = blockIdx.x;
                 pc->t = 0;

@@ -576,9 +576,11 @@ FusedParams fused_params(const petto_ctx* ctx, const StepCoef& k, int cur, int p
 
 // The fused 3D elasticity step (k_elastic3d_fast): one step, or with nloc > 1 a
 // persistent launch of steps step .. step + nloc - 1 (single domain, output =
-// st[prev], no r^2 partials).
+// st[prev], no r^2 partials).  With `rot` (the tolerance loop's buffer rotation:
+// u_it in st[rot[it % 3]]) a persistent launch of the tolerance loop's
+// iterations step .. step + nloc - 1 with the stop test on the device.
 int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next, long long step,
-              long long nsteps, double* partials, int nloc) {
+              long long nsteps, double* partials, int nloc, const int* rot = nullptr) {
     const Geo& g = ctx->g;
     cudaEvent_t ev[2];
     const long long owned = owned_nodes(ctx);
@@ -640,7 +642,20 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
     P.nstrips = (g.ny + e3::W - 1) / e3::W;
     int grid = 0;
     plan_3d(ctx, P.nstrips, P.chunk, P.nitems, grid);
-    if (partials && grid > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
+    if (partials && grid * (rot ? 2 : 1) > ctx->npartials) return fail(ctx, PETTO_ERROR, "partials buffer too small");
+    e3::MapSet<3> MT;  // tolerance loop: iteration it reads st[rot[it % 3]], st[rot[(it + 2) % 3]]
+    if (rot) {
+        for (int j = 0; j < 3; ++j) {
+            MT.m[j].u = ctx->tU[rot[j]];
+            MT.m[j].c = ctx->tC;
+            MT.m[j].p = ctx->tP[rot[(j + 2) % 3]];
+            MT.m[j].m = ctx->tM;
+            MT.m[j].o = ctx->tO[rot[(j + 1) % 3]];
+        }
+        P.nloc = nloc;
+        P.gbar = ctx->gbar;
+        CK(cudaMemsetAsync(ctx->gbar, 0, sizeof(unsigned), ctx->stream));
+    }
     e3::MapSet<2> MS;
     int ob = next == ctx->r ? 3 : -1;
     for (int b = 0; b < 3; ++b)
@@ -651,7 +666,7 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
     MS.m[0].p = ctx->tP[prev];
     MS.m[0].m = ctx->tM;
     MS.m[0].o = ctx->tO[ob];
-    if (nloc > 1) {
+    if (nloc > 1 && !rot) {
         // u_{n+1} overwrites u_{n-1}; the next step reads it as u_n
         if (ob != prev || partials || ctx->peer_step) return fail(ctx, PETTO_ERROR, "persistent 3D launch: bad plan");
         MS.m[1] = MS.m[0];
@@ -676,7 +691,7 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
     // and not on slab ranks, whose steps are separated by stream memory
     // operations.
     cudaLaunchAttribute la[1];
-    if (nloc > 1) {  // every CTA resident (the grid barrier), or the launch fails
+    if (nloc > 1 || rot) {  // every CTA resident (the grid barrier), or the launch fails
         la[0].id = cudaLaunchAttributeCooperative;
         la[0].val.cooperative = 1;
         cfg.attrs = la;
@@ -689,11 +704,17 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
     }
     cudaError_t le;
     // r^2 partials only when a caller reads them (iterate_to_tolerance, residual)
-    if (nloc > 1) {
+    if (rot) {
         switch (k.form) {
-            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<0>, P, MS); break;
-            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<1>, P, MS); break;
-            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<2>, P, MS); break;
+            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<0, true>, P, MT); break;
+            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<1, true>, P, MT); break;
+            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<2, true>, P, MT); break;
+        }
+    } else if (nloc > 1) {
+        switch (k.form) {
+            case 0: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<0, false>, P, MS); break;
+            case 1: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<1, false>, P, MS); break;
+            default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_persist<2, false>, P, MS); break;
         }
     } else
     switch (k.form * 2 + (partials ? 1 : 0)) {
@@ -707,7 +728,7 @@ int e3_launch(petto_ctx* ctx, const StepCoef& k, int cur, int prev, double* next
         default: le = cudaLaunchKernelEx(&cfg, e3::k_elastic3d_fast<3, true>, P, MS.m[0]); break;
     }
     if (le != cudaSuccess) return fail(ctx, PETTO_ERROR, std::string("fused 3D launch: ") + cudaGetErrorString(le));
-    timing_end(ctx, ev, nloc > 1 ? "k_elastic3d_persist" : "k_elastic3d_fast",
+    timing_end(ctx, ev, nloc > 1 || rot ? "k_elastic3d_persist" : "k_elastic3d_fast",
                (double)owned * step_bytes(ctx, k.form) * nloc);
     ctx->launches++;
     CKL();
@@ -1139,9 +1160,12 @@ int petto_dev_create(const petto_grid_desc* d, petto_ctx** out) {
         cudaFuncSetAttribute(E3_KERNEL<2, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(E3_KERNEL<3, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(E3_KERNEL<3, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_persist<0>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_persist<1>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(e3::k_elastic3d_persist<2>, smattr, e3::SMEM_BYTES) != cudaSuccess)
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<0, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<1, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<2, false>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<0, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<1, true>, smattr, e3::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(e3::k_elastic3d_persist<2, true>, smattr, e3::SMEM_BYTES) != cudaSuccess)
         return cleanup("cannot configure shared memory for k_elastic3d_fast");
     if (reset_status(ctx)) return cleanup(ctx->err);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup("device initialisation failed");
@@ -2079,7 +2103,17 @@ int team_iterate_to_tolerance(Team t, int mode, const petto_pt_params* p, double
     auto sumsq = [](petto_ctx* x) -> double* { return &x->status->sumsq; };
     long long launched = 0;  // residual evaluations issued
     long long chunk = 32;
-    while (true) {
+    const bool persist = t.n == 1 && persistent_3d_ok(ctx);
+    while (persist) {
+        // persistent launches of up to 16384 iterations, the stop test inside
+        const long long n = std::min<long long>(max_iters + 1 - launched, 16384);
+        if (int rc = e3_launch(ctx, k, 0, 0, ctx->st[b[0][1]], launched, never, ctx->partials, (int)n, b[0].data()))
+            return rc;
+        launched += n;
+        if (int rc = read_status(ctx)) return rc;
+        if (ctx->status_h->done || launched > max_iters) break;
+    }
+    while (!persist) {
         for (long long c = 0; c < chunk && launched <= max_iters; ++c, ++launched) {
             const long long it = launched;
             for (int i = 0; i < t.n; ++i) {

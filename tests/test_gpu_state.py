@@ -556,3 +556,44 @@ def test_iterate_to_tolerance_divergence_abort(port, mode, c):
     with pytest.raises(D.NumericalAbort) as ei:
         D.iterate_to_tolerance(hist, op, 0, p, 1e-30, 1000)
     assert ei.value.step == want.iterations
+
+
+def _elastic3d_tol(g, E, f, bc, u0, p, target, max_iters, multi):
+    import os
+
+    old = os.environ.get("PETTO_MULTI")
+    os.environ["PETTO_MULTI"] = "1" if multi else "0"
+    try:
+        op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=FAST)
+    finally:
+        if old is None:
+            del os.environ["PETTO_MULTI"]
+        else:
+            os.environ["PETTO_MULTI"] = old
+    hist = D.StateHistory(u0.copy(), u0.copy())
+    st = D.iterate_to_tolerance(hist, op, 1, p, target, max_iters)
+    return hist, st
+
+
+@pytest.mark.parametrize("gi,form,rel_target,max_iters", [(0, 1, 0.05, 5000), (1, 0, 0.2, 3000), (0, 1, 1e-9, 150),
+                                                          (2, 1, 0.05, 20000)])
+def test_elastic3d_persistent_tolerance_matches_per_step(gi, form, rel_target, max_iters):
+    """iterate_to_tolerance in persistent launches (the stop test on the device after
+    a grid barrier) against one launch per iteration + k_iter_finish: the same
+    iterations, residual norms and state, bit for bit -- converged, and stopped by
+    max_iters (third case)."""
+    g = [P.Grid.make3d(12, 9, 10, 2.0, 1.0, 1.0), P.Grid.make3d(70, 23, 19, 2.0, 1.0, 1.0),
+         P.Grid.make3d(128, 64, 64, 1.0, 1.0, 1.0)][gi]
+    E, _, _, f, bc = elastic_case(g, 0)
+    h = g.min_spacing()
+    p = P.PTParams(dt_pt=h * h / 8, dt_apt=0.2 * h, theta=1.0, form=form)
+    z = np.zeros(3 * g.num_nodes)
+    op = D.ElasticityOperator(g, E, 0.3, f, bc, mode=FAST)
+    r0 = op.residual(z)
+    target = rel_target * np.sqrt(np.sum(r0 ** 2)) / g.num_nodes
+    a, sa = _elastic3d_tol(g, E, f, bc, z, p, target, max_iters, True)
+    b, sb = _elastic3d_tol(g, E, f, bc, z, p, target, max_iters, False)
+    assert (sa.iterations, sa.converged, sa.r_initial, sa.r_final) == (sb.iterations, sb.converged, sb.r_initial,
+                                                                       sb.r_final)
+    assert sa.converged == (rel_target > 1e-6)
+    assert np.array_equal(a.current, b.current) and np.array_equal(a.previous, b.previous)
