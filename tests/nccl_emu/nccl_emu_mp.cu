@@ -52,7 +52,6 @@ struct Box {                     // a ring of NMSG messages
 };
 struct Shared {
     std::atomic<int> arrived;
-    std::atomic<int> left;
     Slot slot[MAXR];
     Box box[MAXR][MAXR];   // [sender][receiver]
 };
@@ -258,6 +257,9 @@ ncclResult_t ncclCommInitRank(ncclComm_t* out, int nranks, ncclUniqueId id, int 
         usleep(100);
         if (time(nullptr) - t0 > 120) return ncclSystemError;
     }
+    // every rank has mapped the file: drop its name (nothing is left in /tmp, even
+    // when a rank process exits without destroying its communicator)
+    if (rank == 0) unlink(c->path.c_str());
     *out = reinterpret_cast<ncclComm_t>(c);
     return ncclSuccess;
 }
@@ -265,7 +267,6 @@ ncclResult_t ncclCommInitRank(ncclComm_t* out, int nranks, ncclUniqueId id, int 
 ncclResult_t ncclCommDestroy(ncclComm_t comm) {
     Comm* c = reinterpret_cast<Comm*>(comm);
     if (!c) return ncclSuccess;
-    if (c->sh->left.fetch_add(1) + 1 == c->n) unlink(c->path.c_str());
     munmap(c->sh, sizeof(Shared));
     delete c;
     return ncclSuccess;
